@@ -1,0 +1,859 @@
+// libaco_gpu.so — C-ABI implementation (include/aco_gpu.h).
+//
+// One context = one GPU = one colony shard.  All iteration state (tau,
+// choice, tours, lengths, best tour) stays resident in HBM/L2; the host only
+// sees what the caller asks for.  Multi-GPU sharding uses NCCL,
+// loaded at run time with dlopen so a single-GPU process never needs it.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "../../include/aco_gpu.h"
+#include "construct.cuh"
+#include "host_model.hpp"
+#include "update.cuh"
+
+using namespace acob200;
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved lazily.
+namespace {
+
+struct NcclApi {
+    bool loaded = false;
+    void* handle = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    if (!api.loaded) {
+        api.loaded = true;
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            api.handle = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (api.handle) break;
+        }
+        if (api.handle) {
+            auto sym = [&](const char* s) { return dlsym(api.handle, s); };
+            api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+            api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+            api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+            api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+            api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+            api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
+            api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+            api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+            api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+        }
+    }
+    return api;
+}
+
+thread_local std::string g_host_err;
+
+struct Fail {
+    aco_status code;
+    std::string msg;
+};
+
+} // namespace
+
+// ---------------------------------------------------------------------------
+struct aco_gpu_ctx {
+    // configuration
+    Config cfg;
+    int n = 0, m = 0, stream_kind = ACO_STREAM_FP32;
+    uint64_t seed = 1;
+    int random_start = 0;
+    int rank = 0, world = 1, ant_begin = 0, ant_end = 0, mloc = 0, S = 0;
+    int P64 = 0, PW = 0, NV = 0, V = 4, C = 0, R = 1, MAXR = 1, tabu_words = 0;
+    double tau0 = 0.0;
+    int64_t max_d = 0;
+    int device = 0, num_sms = 0;
+    int construct_grid = 0;
+    int iteration = 0;
+    int64_t best_so_far = std::numeric_limits<int64_t>::max();
+    int64_t launches = 0;
+    std::string err;
+
+    // device buffers
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[6] = {};
+    int32_t* d_dist = nullptr;
+    double* d_lut = nullptr;
+    double* d_etab = nullptr;
+    double* d_tau = nullptr;
+    double* d_choice = nullptr;
+    float* d_choice32 = nullptr;
+    double* d_choice_p64 = nullptr;
+    int32_t* d_scale = nullptr;
+    int32_t* d_nn = nullptr;
+    int32_t* d_tours = nullptr;
+    int64_t* d_len = nullptr;
+    double* d_inv = nullptr;   // [world][S]
+    int32_t* d_succ = nullptr; // [world][n][S]
+    int32_t* d_pred = nullptr;
+    double* d_delta = nullptr;
+    long long* d_stats = nullptr;   // [0..2] stats, [3] best_so_far
+    int32_t* d_best = nullptr;      // n+1
+    unsigned long long* d_fb = nullptr; // [0] roulette fallbacks, [1] nn argmax fallbacks
+    long long* h_stats = nullptr;       // pinned: 4 stats + 2 fallback counters
+    ncclComm_t comm = nullptr;
+};
+
+namespace {
+
+#define CK(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            throw Fail{ACO_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};  \
+    } while (0)
+
+#define NK(call)                                                                         \
+    do {                                                                                 \
+        ncclResult_t r_ = (call);                                                        \
+        if (r_ != ncclSuccess)                                                           \
+            throw Fail{ACO_E_NCCL, std::string(#call) + ": " +                           \
+                                       (nccl().GetErrorString ? nccl().GetErrorString(r_) \
+                                                              : "nccl error")};          \
+    } while (0)
+
+template <class F>
+aco_status guard_ctx(aco_gpu_ctx* ctx, F&& f) {
+    try {
+        f();
+        return ACO_OK;
+    } catch (const Fail& e) {
+        if (ctx) ctx->err = e.msg;
+        g_host_err = e.msg;
+        return e.code;
+    } catch (const ModelError& e) {
+        if (ctx) ctx->err = e.what();
+        g_host_err = e.what();
+        return static_cast<aco_status>(1 + static_cast<int>(e.code));
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        g_host_err = e.what();
+        return ACO_E_CUDA;
+    }
+}
+
+void check_launch(aco_gpu_ctx* c, const char* what) {
+    ++c->launches;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Fail{ACO_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+int round_up(int x, int a) { return (x + a - 1) / a * a; }
+
+__global__ void k_fill(double* p, size_t count, double v) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+// ---- construction kernel dispatch ------------------------------------------
+using ConstructFn = void (*)(ConstructParams);
+
+template <typename WT>
+ConstructFn pick_roulette(int NV, int MAXR) {
+    if (MAXR == 1) {
+        switch (NV) {
+        case 2: return k_construct_roulette<WT, 2, 1>;
+        case 4: return k_construct_roulette<WT, 4, 1>;
+        case 8: return k_construct_roulette<WT, 8, 1>;
+        case 12: return k_construct_roulette<WT, 12, 1>;
+        case 16: return k_construct_roulette<WT, 16, 1>;
+        default: return k_construct_roulette<WT, 20, 1>;
+        }
+    }
+    return k_construct_roulette<WT, 20, 8>;
+}
+
+void choose_stream_layout(aco_gpu_ctx* c) {
+    c->V = (c->stream_kind == ACO_STREAM_FP64) ? 2 : 4;
+    static const int nvs[] = {2, 4, 8, 12, 16, 20};
+    c->NV = 0;
+    for (int nv : nvs)
+        if (32 * nv * c->V >= c->n) {
+            c->NV = nv;
+            break;
+        }
+    if (c->NV) {
+        c->MAXR = 1;
+        c->R = 1;
+    } else {
+        c->NV = 20;
+        c->MAXR = 8;
+        c->R = (c->n + 32 * 20 * c->V - 1) / (32 * 20 * c->V);
+        if (c->R > 8)
+            throw Fail{ACO_E_UNSUPPORTED, "full-row roulette supports n <= " +
+                                              std::to_string(8 * 32 * 20 * c->V) +
+                                              " with this weight stream"};
+    }
+    c->C = c->NV * c->V;
+    c->PW = c->R * 32 * c->C;
+    c->tabu_words = c->PW / 32 + 4;
+}
+
+void launch_rows(aco_gpu_ctx* c, int mode) {
+    RowParams rp{};
+    rp.tau = c->d_tau;
+    rp.choice64 = c->d_choice;
+    rp.choice32 = c->d_choice32;
+    rp.choice_perm64 = c->d_choice_p64;
+    rp.scale_exp = c->d_scale;
+    rp.dist = c->d_dist;
+    rp.lut = c->d_lut;
+    rp.etab = c->d_etab;
+    rp.delta = c->d_delta;
+    rp.succ = c->d_succ;
+    rp.pred = c->d_pred;
+    rp.inv = c->d_inv;
+    rp.n = c->n;
+    rp.P64 = c->P64;
+    rp.PW = c->PW;
+    rp.C = c->C;
+    rp.V = c->V;
+    rp.shards = c->world;
+    rp.S = c->S;
+    rp.m = c->world == 1 ? c->mloc : c->m; // a local ant range is one shard of mloc ants
+    rp.alpha = c->cfg.alpha;
+    rp.keep = 1.0 - c->cfg.rho; // pheromone.hpp:179
+    const size_t smem = static_cast<size_t>(c->P64) * sizeof(double);
+    const int grid = std::min(c->n, c->num_sms * 8);
+    if (mode == MODE_CHOICE) k_rows<MODE_CHOICE><<<grid, 256, smem, c->stream>>>(rp);
+    else if (mode == MODE_GATHER) k_rows<MODE_GATHER><<<grid, 256, smem, c->stream>>>(rp);
+    else k_rows<MODE_DELTA><<<grid, 256, smem, c->stream>>>(rp);
+    check_launch(c, "k_rows");
+}
+
+ConstructParams make_cp(aco_gpu_ctx* c) {
+    ConstructParams p{};
+    p.w = c->stream_kind == ACO_STREAM_FP64 ? static_cast<const void*>(c->d_choice_p64)
+                                            : static_cast<const void*>(c->d_choice32);
+    p.w64 = c->d_choice;
+    p.nn_lists = c->d_nn;
+    p.tours = c->d_tours;
+    p.fallbacks = c->d_fb;
+    p.argmax_fallbacks = c->d_fb + 1;
+    p.n = c->n;
+    p.P64 = c->P64;
+    p.PW = c->PW;
+    p.R = c->R;
+    p.nn = c->cfg.nn;
+    p.ant_begin = c->ant_begin;
+    p.mloc = c->mloc;
+    p.random_start = c->random_start;
+    p.theta = c->cfg.theta;
+    p.tabu_words = c->tabu_words;
+    p.iteration = static_cast<uint32_t>(c->iteration);
+    p.seed = c->seed;
+    return p;
+}
+
+void launch_construct(aco_gpu_ctx* c) {
+    ConstructParams p = make_cp(c);
+    const size_t smem1 = static_cast<size_t>(c->tabu_words) * sizeof(uint32_t);
+    if (c->mloc == 0) return;
+    if (c->cfg.selection == ACO_SEL_ROULETTE) {
+        ConstructFn fn = c->stream_kind == ACO_STREAM_FP64 ? pick_roulette<double>(c->NV, c->MAXR)
+                                                           : pick_roulette<float>(c->NV, c->MAXR);
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem1));
+        const int grid = std::max(1, std::min(c->mloc, per_sm * c->num_sms));
+        c->construct_grid = grid;
+        fn<<<grid, 32, smem1, c->stream>>>(p);
+        check_launch(c, "k_construct_roulette");
+    } else if (c->cfg.selection == ACO_SEL_NN) {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_construct_nn, 32, smem1));
+        const int grid = std::max(1, std::min(c->mloc, per_sm * c->num_sms));
+        c->construct_grid = grid;
+        k_construct_nn<<<grid, 32, smem1, c->stream>>>(p);
+        check_launch(c, "k_construct_nn");
+    } else {
+        const size_t smem4 = smem1 * 4;
+        const int grid = std::max(1, (c->mloc + 3) / 4);
+        c->construct_grid = grid;
+        k_construct_data_parallel<<<grid, 128, smem4, c->stream>>>(p);
+        check_launch(c, "k_construct_data_parallel");
+    }
+}
+
+bool gather_mode(const aco_gpu_ctx* c) { return c->cfg.deposit != ACO_DEP_ACCUMULATE; }
+
+// construction + tour lengths + iteration stats (no host sync)
+void do_construct(aco_gpu_ctx* c) {
+    CK(cudaMemsetAsync(c->d_fb, 0, 2 * sizeof(unsigned long long), c->stream));
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    launch_construct(c);
+    CK(cudaEventRecord(c->ev[1], c->stream));
+    {
+        const int warps = 8;
+        const int grid = std::max(1, std::min((c->mloc + warps - 1) / warps, c->num_sms * 16));
+        int32_t* succ = nullptr;
+        int32_t* pred = nullptr;
+        if (gather_mode(c)) {
+            succ = c->d_succ + static_cast<size_t>(c->rank) * c->n * c->S;
+            pred = c->d_pred + static_cast<size_t>(c->rank) * c->n * c->S;
+        }
+        k_tour_length<<<grid, 32 * warps, 0, c->stream>>>(
+            c->d_tours, c->d_dist, c->n, c->P64, c->mloc, c->d_len,
+            c->d_inv + static_cast<size_t>(c->rank) * c->S, succ, pred, c->S);
+        check_launch(c, "k_tour_length");
+    }
+    // world == 1: stats kernel also maintains best-so-far on device.
+    k_iter_stats<<<1, 1024, 0, c->stream>>>(
+        c->d_len, c->mloc, c->d_tours, c->n, c->d_stats, c->d_stats + 3, c->d_best,
+        c->world == 1 ? 1 : 0);
+    check_launch(c, "k_iter_stats");
+    CK(cudaEventRecord(c->ev[2], c->stream));
+}
+
+// exchange + evaporate + deposit + choice (no host sync)
+void do_update(aco_gpu_ctx* c) {
+    const double keep = 1.0 - c->cfg.rho;
+    if (c->world > 1) {
+        auto& api = nccl();
+        if (gather_mode(c)) {
+            const size_t blk = static_cast<size_t>(c->n) * c->S;
+            NK(api.GroupStart());
+            NK(api.AllGather(c->d_succ + c->rank * blk, c->d_succ, blk, ncclInt32, c->comm, c->stream));
+            NK(api.AllGather(c->d_pred + c->rank * blk, c->d_pred, blk, ncclInt32, c->comm, c->stream));
+            NK(api.AllGather(c->d_inv + static_cast<size_t>(c->rank) * c->S, c->d_inv, c->S,
+                             ncclFloat64, c->comm, c->stream));
+            NK(api.GroupEnd());
+        } else {
+            k_deposit_atomic<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_tours, c->d_inv + static_cast<size_t>(c->rank) * c->S,
+                                                                    c->n, c->P64, c->mloc, c->d_delta);
+            check_launch(c, "k_deposit_atomic");
+            NK(api.AllReduce(c->d_delta, c->d_delta, static_cast<size_t>(c->n) * c->P64,
+                             ncclFloat64, ncclSum, c->comm, c->stream));
+        }
+    }
+    CK(cudaEventRecord(c->ev[3], c->stream));
+    if (gather_mode(c)) {
+        launch_rows(c, MODE_GATHER);
+        CK(cudaEventRecord(c->ev[4], c->stream));
+    } else if (c->world > 1) {
+        launch_rows(c, MODE_DELTA);
+        CK(cudaEventRecord(c->ev[4], c->stream));
+    } else {
+        const size_t count2 = static_cast<size_t>(c->n) * c->P64 / 2;
+        k_evaporate<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_tau, count2, keep);
+        check_launch(c, "k_evaporate");
+        k_deposit_atomic<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_tours, c->d_inv, c->n, c->P64,
+                                                                c->mloc, c->d_tau);
+        check_launch(c, "k_deposit_atomic");
+        CK(cudaEventRecord(c->ev[4], c->stream));
+        launch_rows(c, MODE_CHOICE);
+    }
+    CK(cudaEventRecord(c->ev[5], c->stream));
+}
+
+float ev_ms(aco_gpu_ctx* c, int a, int b) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]));
+    return ms;
+}
+
+// Reads stats; for world > 1 reduces them over NCCL (best, then owner, sum)
+// and broadcasts the improving tour.
+void finish_stats(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
+    if (c->world > 1) {
+        auto& api = nccl();
+        long long* s = c->d_stats;
+        // s[0] best len (local), s[1] best local ant, s[2] sum.
+        // scratch: s[4] global best, s[5] owner key, s[6] global sum
+        CK(cudaMemcpyAsync(s + 4, s, sizeof(long long), cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemcpyAsync(s + 6, s + 2, sizeof(long long), cudaMemcpyDeviceToDevice, c->stream));
+        NK(api.GroupStart());
+        NK(api.AllReduce(s + 4, s + 4, 1, ncclInt64, ncclMin, c->comm, c->stream));
+        NK(api.AllReduce(s + 6, s + 6, 1, ncclInt64, ncclSum, c->comm, c->stream));
+        NK(api.GroupEnd());
+        CK(cudaMemcpyAsync(c->h_stats, s, 7 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        const long long gbest = c->h_stats[4];
+        long long key = c->h_stats[0] == gbest ? c->ant_begin + c->h_stats[1] : LLONG_MAX;
+        CK(cudaMemcpyAsync(s + 5, &key, sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+        NK(api.AllReduce(s + 5, s + 5, 1, ncclInt64, ncclMin, c->comm, c->stream));
+        CK(cudaMemcpyAsync(c->h_stats + 5, s + 5, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        const long long owner_ant = c->h_stats[5];
+        const int owner = static_cast<int>(owner_ant / c->S);
+        rec->best_length = gbest;
+        rec->mean_length = static_cast<double>(c->h_stats[6]) / static_cast<double>(c->m);
+        if (gbest < c->best_so_far) {
+            c->best_so_far = gbest;
+            if (c->rank == owner) {
+                const int local = static_cast<int>(owner_ant - c->ant_begin);
+                CK(cudaMemcpyAsync(c->d_best, c->d_tours + static_cast<size_t>(local) * (c->n + 1),
+                                   sizeof(int32_t) * (c->n + 1), cudaMemcpyDeviceToDevice, c->stream));
+            }
+            NK(api.Broadcast(c->d_best, c->d_best, c->n + 1, ncclInt32, owner, c->comm, c->stream));
+        }
+    } else {
+        rec->best_length = c->h_stats[0];
+        rec->mean_length = static_cast<double>(c->h_stats[2]) / static_cast<double>(c->mloc);
+        c->best_so_far = std::min<int64_t>(c->best_so_far, c->h_stats[0]);
+    }
+}
+
+void fill_common(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
+    rec->iteration = c->iteration + 1;
+    predicted_access_cost(c->cfg.deposit, c->n, c->m, c->cfg.theta, rec->ledger);
+}
+
+} // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* aco_errc_name(int s) {
+    static const char* names[] = {"ok", "missing_field", "unsupported_edge_weight_type",
+                                  "malformed_coord", "dimension_mismatch", "index_out_of_range",
+                                  "overflow", "invalid_length", "not_a_permutation", "not_closed",
+                                  "all_visited", "inconsistent_length", "io_error", "config_error"};
+    if (s >= 0 && s <= 13) return names[s];
+    if (s == ACO_E_CUDA) return "cuda_error";
+    if (s == ACO_E_NCCL) return "nccl_error";
+    if (s == ACO_E_UNSUPPORTED) return "unsupported";
+    return "unknown";
+}
+
+const char* aco_last_error(void) { return g_host_err.c_str(); }
+
+aco_status aco_parse_instance(const char* text, int32_t* dimension, int32_t* ewt, double* xs,
+                              double* ys, int32_t capacity, char* name, int32_t name_capacity) {
+    return guard_ctx(nullptr, [&] {
+        Instance in;
+        parse_instance(text ? std::string_view(text) : std::string_view(), in);
+        *dimension = in.dimension;
+        if (ewt) *ewt = in.edge_weight_type;
+        if (xs && ys && capacity >= in.dimension) {
+            std::copy(in.xs.begin(), in.xs.end(), xs);
+            std::copy(in.ys.begin(), in.ys.end(), ys);
+        }
+        if (name && name_capacity > 0) {
+            std::snprintf(name, static_cast<size_t>(name_capacity), "%s", in.name.c_str());
+        }
+    });
+}
+
+aco_status aco_parse_tour(const char* text, int32_t* tour, int32_t capacity, int32_t* length) {
+    return guard_ctx(nullptr, [&] {
+        const auto t = parse_tour(text ? std::string_view(text) : std::string_view());
+        *length = static_cast<int32_t>(t.size());
+        for (int i = 0; i < static_cast<int>(t.size()) && i < capacity; ++i) tour[i] = t[i];
+    });
+}
+
+aco_status aco_build_distances(int32_t n, const double* xs, const double* ys, int32_t ewt,
+                               int32_t* dist) {
+    return guard_ctx(nullptr, [&] { build_distances(n, xs, ys, ewt, dist); });
+}
+
+aco_status aco_build_nn_lists(int32_t n, const int32_t* dist, int32_t nn, int32_t* out) {
+    return guard_ctx(nullptr, [&] { build_nn_lists(n, dist, nn, out); });
+}
+
+aco_status aco_greedy_tour_length(int32_t n, const int32_t* dist, int64_t* out) {
+    return guard_ctx(nullptr, [&] { *out = greedy_tour_length(n, dist); });
+}
+
+aco_status aco_tour_length(int32_t n, const int32_t* dist, const int32_t* tour, int32_t len,
+                           int64_t* out) {
+    return guard_ctx(nullptr, [&] { *out = tour_length(n, dist, tour, len); });
+}
+
+aco_status aco_predicted_access_cost(int32_t deposit, int32_t n, int32_t m, int32_t theta,
+                                     double out[4]) {
+    return guard_ctx(nullptr, [&] {
+        if (deposit < 0 || deposit > 3) throw ModelError(Errc::config_error, "unknown deposit strategy");
+        predicted_access_cost(deposit, n, m, theta, out);
+    });
+}
+
+aco_status aco_gpu_nccl_unique_id(uint8_t out[128]) {
+    return guard_ctx(nullptr, [&] {
+        auto& api = nccl();
+        if (!api.GetUniqueId) throw Fail{ACO_E_NCCL, "libnccl.so.2 not found"};
+        ncclUniqueId id;
+        NK(api.GetUniqueId(&id));
+        static_assert(sizeof(id) == 128, "nccl id size");
+        std::memcpy(out, &id, 128);
+    });
+}
+
+aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gpu_ctx** out) {
+    if (!out) return ACO_E_CONFIG_ERROR;
+    *out = nullptr;
+    auto* c = new aco_gpu_ctx;
+    const aco_status st = guard_ctx(c, [&] {
+        if (!prm || !dist) throw ModelError(Errc::config_error, "params and dist are required");
+        if (prm->n < 2) throw ModelError(Errc::dimension_mismatch, "n must be at least 2");
+        c->cfg.n = c->n = prm->n;
+        c->cfg.m = prm->m == 0 ? prm->n : prm->m; // engine.hpp:60
+        c->cfg.nn = prm->nn;
+        c->cfg.theta = prm->theta;
+        c->cfg.selection = prm->selection;
+        c->cfg.deposit = prm->deposit;
+        c->cfg.alpha = prm->alpha;
+        c->cfg.beta = prm->beta;
+        c->cfg.rho = prm->rho;
+        validate(c->cfg);
+        if (c->cfg.m < 1) throw ModelError(Errc::config_error, "ant count must be >= 1");
+        c->m = c->cfg.m;
+        c->seed = prm->seed;
+        c->random_start = prm->random_start;
+        c->stream_kind = prm->stream == ACO_STREAM_FP64 ? ACO_STREAM_FP64 : ACO_STREAM_FP32;
+        c->world = prm->world > 1 ? prm->world : 1;
+        c->rank = c->world > 1 ? prm->rank : 0;
+        if (c->rank < 0 || c->rank >= c->world) throw ModelError(Errc::config_error, "bad rank");
+        c->S = (c->m + c->world - 1) / c->world;
+        if (c->world == 1 && (prm->ant_begin != 0 || prm->ant_end != 0)) {
+            if (!(0 <= prm->ant_begin && prm->ant_begin < prm->ant_end && prm->ant_end <= c->m))
+                throw ModelError(Errc::config_error, "bad ant range");
+            c->ant_begin = prm->ant_begin;
+            c->ant_end = prm->ant_end;
+            c->S = c->ant_end - c->ant_begin;
+        } else {
+            c->ant_begin = std::min(c->m, c->rank * c->S);
+            c->ant_end = std::min(c->m, (c->rank + 1) * c->S);
+        }
+        c->mloc = c->ant_end - c->ant_begin;
+        c->device = prm->device;
+
+        // host model: distances, eta^beta table, tau0, nn lists
+        const int n = c->n;
+        for (size_t i = 0; i < static_cast<size_t>(n) * n; ++i) {
+            if (dist[i] < 0) throw ModelError(Errc::overflow, "negative distance");
+            c->max_d = std::max<int64_t>(c->max_d, dist[i]);
+        }
+        if (c->max_d > 0 && static_cast<int64_t>(n) > std::numeric_limits<int64_t>::max() / c->max_d)
+            throw ModelError(Errc::overflow, "tour lengths would overflow 64-bit range");
+        c->tau0 = static_cast<double>(c->m) / static_cast<double>(greedy_tour_length(n, dist));
+        std::vector<int32_t> nn_host;
+        if (c->cfg.selection == ACO_SEL_NN) {
+            nn_host.resize(static_cast<size_t>(n) * c->cfg.nn);
+            build_nn_lists(n, dist, c->cfg.nn, nn_host.data());
+        }
+
+        // device
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        if (c->device < 0 || c->device >= ndev) throw Fail{ACO_E_CUDA, "no such CUDA device"};
+        CK(cudaSetDevice(c->device));
+        CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        for (auto& e : c->ev) CK(cudaEventCreate(&e));
+        choose_stream_layout(c);
+        c->P64 = round_up(n, 32);
+        const size_t cells = static_cast<size_t>(n) * c->P64;
+        CK(cudaMalloc(&c->d_dist, cells * sizeof(int32_t)));
+        CK(cudaMemset(c->d_dist, 0, cells * sizeof(int32_t)));
+        CK(cudaMemcpy2D(c->d_dist, c->P64 * sizeof(int32_t), dist, n * sizeof(int32_t),
+                        n * sizeof(int32_t), n, cudaMemcpyHostToDevice));
+        if (c->max_d <= (1 << 25)) {
+            const std::vector<double> lut = eta_beta_table(c->max_d, c->cfg.beta);
+            CK(cudaMalloc(&c->d_lut, lut.size() * sizeof(double)));
+            CK(cudaMemcpy(c->d_lut, lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice));
+        } else {
+            // very long edges: a dense eta^beta matrix instead of a table
+            std::vector<double> et(cells, 0.0);
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j) {
+                    const int32_t d = dist[static_cast<size_t>(i) * n + j];
+                    const double eta = d > 0 ? 1.0 / d : 1.0;
+                    et[static_cast<size_t>(i) * c->P64 + j] = std::pow(eta, c->cfg.beta);
+                }
+            CK(cudaMalloc(&c->d_etab, cells * sizeof(double)));
+            CK(cudaMemcpy(c->d_etab, et.data(), cells * sizeof(double), cudaMemcpyHostToDevice));
+        }
+        CK(cudaMalloc(&c->d_tau, cells * sizeof(double)));
+        CK(cudaMemset(c->d_tau, 0, cells * sizeof(double)));
+        CK(cudaMalloc(&c->d_choice, cells * sizeof(double)));
+        CK(cudaMemset(c->d_choice, 0, cells * sizeof(double)));
+        const size_t wcells = static_cast<size_t>(n) * c->PW;
+        if (c->cfg.selection == ACO_SEL_ROULETTE) {
+            if (c->stream_kind == ACO_STREAM_FP32) {
+                CK(cudaMalloc(&c->d_choice32, wcells * sizeof(float)));
+                CK(cudaMemset(c->d_choice32, 0, wcells * sizeof(float)));
+            } else {
+                CK(cudaMalloc(&c->d_choice_p64, wcells * sizeof(double)));
+                CK(cudaMemset(c->d_choice_p64, 0, wcells * sizeof(double)));
+            }
+        }
+        CK(cudaMalloc(&c->d_scale, n * sizeof(int32_t)));
+        CK(cudaMemset(c->d_scale, 0, n * sizeof(int32_t)));
+        if (!nn_host.empty()) {
+            CK(cudaMalloc(&c->d_nn, nn_host.size() * sizeof(int32_t)));
+            CK(cudaMemcpy(c->d_nn, nn_host.data(), nn_host.size() * sizeof(int32_t),
+                          cudaMemcpyHostToDevice));
+        }
+        const size_t ml = std::max(1, c->mloc);
+        CK(cudaMalloc(&c->d_tours, ml * (n + 1) * sizeof(int32_t)));
+        CK(cudaMemset(c->d_tours, 0, ml * (n + 1) * sizeof(int32_t)));
+        CK(cudaMalloc(&c->d_len, ml * sizeof(int64_t)));
+        CK(cudaMalloc(&c->d_inv, static_cast<size_t>(c->world) * c->S * sizeof(double)));
+        if (c->cfg.deposit != ACO_DEP_ACCUMULATE) {
+            const size_t sp = static_cast<size_t>(c->world) * n * c->S;
+            CK(cudaMalloc(&c->d_succ, sp * sizeof(int32_t)));
+            CK(cudaMalloc(&c->d_pred, sp * sizeof(int32_t)));
+        } else if (c->world > 1) {
+            CK(cudaMalloc(&c->d_delta, cells * sizeof(double)));
+            CK(cudaMemset(c->d_delta, 0, cells * sizeof(double)));
+        }
+        CK(cudaMalloc(&c->d_stats, 8 * sizeof(long long)));
+        const long long init_stats[8] = {0, 0, 0, LLONG_MAX, 0, 0, 0, 0};
+        CK(cudaMemcpy(c->d_stats, init_stats, sizeof(init_stats), cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&c->d_best, (n + 1) * sizeof(int32_t)));
+        CK(cudaMemset(c->d_best, 0, (n + 1) * sizeof(int32_t)));
+        CK(cudaMalloc(&c->d_fb, 2 * sizeof(unsigned long long)));
+        CK(cudaMallocHost(&c->h_stats, 8 * sizeof(long long)));
+
+        if (c->world > 1) {
+            auto& api = nccl();
+            if (!api.CommInitRank) throw Fail{ACO_E_NCCL, "libnccl.so.2 not found"};
+            ncclUniqueId id;
+            std::memcpy(&id, prm->nccl_id, sizeof(id));
+            NK(api.CommInitRank(&c->comm, c->world, id, c->rank));
+        }
+
+        // tau0 everywhere (diagonal included, model.hpp:258-262), then choice
+        k_fill<<<c->num_sms * 4, 256, 0, c->stream>>>(c->d_tau, cells, c->tau0);
+        check_launch(c, "k_fill");
+        // pad columns stay zero
+        if (c->P64 != n)
+            CK(cudaMemset2DAsync(c->d_tau + n, c->P64 * sizeof(double), 0,
+                                 (c->P64 - n) * sizeof(double), n, c->stream));
+        launch_rows(c, MODE_CHOICE);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+    if (st != ACO_OK) {
+        aco_gpu_destroy(c);
+        return st;
+    }
+    *out = c;
+    return ACO_OK;
+}
+
+void aco_gpu_destroy(aco_gpu_ctx* c) {
+    if (!c) return;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
+    void* bufs[] = {c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
+                    c->d_choice_p64, c->d_scale, c->d_nn, c->d_tours, c->d_len, c->d_inv,
+                    c->d_succ, c->d_pred, c->d_delta, c->d_stats, c->d_best, c->d_fb};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    if (c->h_stats) cudaFreeHost(c->h_stats);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* aco_gpu_last_error(const aco_gpu_ctx* c) { return c ? c->err.c_str() : g_host_err.c_str(); }
+
+int64_t aco_gpu_launch_count(const aco_gpu_ctx* c) { return c ? c->launches : 0; }
+
+aco_status aco_gpu_set_pheromone(aco_gpu_ctx* c, const double* tau) {
+    return guard_ctx(c, [&] {
+        CK(cudaSetDevice(c->device));
+        CK(cudaMemcpy2DAsync(c->d_tau, c->P64 * sizeof(double), tau, c->n * sizeof(double),
+                             c->n * sizeof(double), c->n, cudaMemcpyHostToDevice, c->stream));
+        launch_rows(c, MODE_CHOICE);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+aco_status aco_gpu_compute_choice_info(aco_gpu_ctx* c) {
+    return guard_ctx(c, [&] {
+        CK(cudaSetDevice(c->device));
+        launch_rows(c, MODE_CHOICE);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+aco_status aco_gpu_construct(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
+    return guard_ctx(c, [&] {
+        CK(cudaSetDevice(c->device));
+        do_construct(c);
+        CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h_stats + 6, c->d_fb, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        aco_gpu_iter_record tmp{};
+        aco_gpu_iter_record* r = rec ? rec : &tmp;
+        const long long fb0 = c->h_stats[6], fb1 = c->h_stats[7];
+        fill_common(c, r);
+        finish_stats(c, r);
+        r->construct_ms = ev_ms(c, 0, 2);
+        r->construct_kernel_ms = ev_ms(c, 0, 1);
+        r->fallbacks = fb0 + fb1;
+        r->best_so_far = c->best_so_far;
+    });
+}
+
+aco_status aco_gpu_update(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
+    return guard_ctx(c, [&] {
+        CK(cudaSetDevice(c->device));
+        do_update(c);
+        CK(cudaStreamSynchronize(c->stream));
+        if (rec) {
+            rec->update_ms = ev_ms(c, 2, 5);
+            rec->exchange_ms = ev_ms(c, 2, 3);
+            rec->choice_ms = (!gather_mode(c) && c->world == 1) ? ev_ms(c, 4, 5) : 0.0;
+        }
+        ++c->iteration;
+    });
+}
+
+aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* tours_out,
+                           int64_t* lengths_out) {
+    return guard_ctx(c, [&] {
+        CK(cudaSetDevice(c->device));
+        aco_gpu_iter_record tmp{};
+        aco_gpu_iter_record* r = rec ? rec : &tmp;
+        fill_common(c, r);
+        do_construct(c);
+        if (c->world > 1) {
+            // stats must be reduced before the best tour can be broadcast
+            CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+            finish_stats(c, r);
+        }
+        do_update(c);
+        if (tours_out)
+            CK(cudaMemcpyAsync(tours_out, c->d_tours, sizeof(int32_t) * c->mloc * (c->n + 1),
+                               cudaMemcpyDeviceToHost, c->stream));
+        if (lengths_out)
+            CK(cudaMemcpyAsync(lengths_out, c->d_len, sizeof(int64_t) * c->mloc,
+                               cudaMemcpyDeviceToHost, c->stream));
+        if (c->world == 1)
+            CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h_stats + 6, c->d_fb, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (c->world == 1) finish_stats(c, r);
+        r->construct_ms = ev_ms(c, 0, 2);
+        r->construct_kernel_ms = ev_ms(c, 0, 1);
+        r->update_ms = ev_ms(c, 2, 5);
+        r->exchange_ms = ev_ms(c, 2, 3);
+        r->choice_ms = (!gather_mode(c) && c->world == 1) ? ev_ms(c, 4, 5) : 0.0;
+        r->fallbacks = c->h_stats[6] + c->h_stats[7];
+        r->best_so_far = c->best_so_far;
+        ++c->iteration;
+    });
+}
+
+aco_status aco_gpu_get_pheromone(aco_gpu_ctx* c, double* tau) {
+    return guard_ctx(c, [&] {
+        CK(cudaSetDevice(c->device));
+        CK(cudaMemcpy2DAsync(tau, c->n * sizeof(double), c->d_tau, c->P64 * sizeof(double),
+                             c->n * sizeof(double), c->n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+aco_status aco_gpu_get_choice(aco_gpu_ctx* c, double* choice) {
+    return guard_ctx(c, [&] {
+        CK(cudaSetDevice(c->device));
+        CK(cudaMemcpy2DAsync(choice, c->n * sizeof(double), c->d_choice, c->P64 * sizeof(double),
+                             c->n * sizeof(double), c->n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+aco_status aco_gpu_get_choice32(aco_gpu_ctx* c, float* choice, int32_t* scale_exp) {
+    return guard_ctx(c, [&] {
+        if (!c->d_choice32) throw Fail{ACO_E_UNSUPPORTED, "fp32 stream not active"};
+        CK(cudaSetDevice(c->device));
+        std::vector<float> raw(static_cast<size_t>(c->n) * c->PW);
+        CK(cudaMemcpy(raw.data(), c->d_choice32, raw.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        if (scale_exp) CK(cudaMemcpy(scale_exp, c->d_scale, c->n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < c->n; ++i)
+            for (int j = 0; j < c->n; ++j)
+                choice[static_cast<size_t>(i) * c->n + j] =
+                    raw[static_cast<size_t>(i) * c->PW + stream_pos(j, c->C, 4)];
+    });
+}
+
+aco_status aco_gpu_get_tours(aco_gpu_ctx* c, int32_t* tours, int64_t* lengths) {
+    return guard_ctx(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (tours)
+            CK(cudaMemcpyAsync(tours, c->d_tours, sizeof(int32_t) * c->mloc * (c->n + 1),
+                               cudaMemcpyDeviceToHost, c->stream));
+        if (lengths)
+            CK(cudaMemcpyAsync(lengths, c->d_len, sizeof(int64_t) * c->mloc, cudaMemcpyDeviceToHost,
+                               c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+aco_status aco_gpu_get_best(aco_gpu_ctx* c, int32_t* tour, int64_t* length) {
+    return guard_ctx(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (tour)
+            CK(cudaMemcpyAsync(tour, c->d_best, sizeof(int32_t) * (c->n + 1), cudaMemcpyDeviceToHost,
+                               c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (length) *length = c->best_so_far;
+    });
+}
+
+aco_status aco_gpu_get_info(aco_gpu_ctx* c, int32_t* m, int32_t* ant_begin, int32_t* ant_end,
+                            double* tau0, int32_t* stream, int32_t* iteration) {
+    if (!c) return ACO_E_CONFIG_ERROR;
+    if (m) *m = c->m;
+    if (ant_begin) *ant_begin = c->ant_begin;
+    if (ant_end) *ant_end = c->ant_end;
+    if (tau0) *tau0 = c->tau0;
+    if (stream) *stream = c->stream_kind;
+    if (iteration) *iteration = c->iteration;
+    return ACO_OK;
+}
+
+aco_status aco_gpu_philox_uniform(int32_t device, uint64_t seed, uint32_t it, uint32_t ant,
+                                  int32_t count, const uint32_t* steps, const uint32_t* draws,
+                                  double* out) {
+    return guard_ctx(nullptr, [&] {
+        CK(cudaSetDevice(device));
+        uint32_t *ds = nullptr, *dd = nullptr;
+        double* dout = nullptr;
+        CK(cudaMalloc(&ds, count * sizeof(uint32_t)));
+        CK(cudaMalloc(&dd, count * sizeof(uint32_t)));
+        CK(cudaMalloc(&dout, count * sizeof(double)));
+        CK(cudaMemcpy(ds, steps, count * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dd, draws, count * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        k_philox_test<<<(count + 255) / 256, 256>>>(seed, it, ant, count, ds, dd, dout);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(out, dout, count * sizeof(double), cudaMemcpyDeviceToHost));
+        cudaFree(ds);
+        cudaFree(dd);
+        cudaFree(dout);
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,270 @@
+// Tour-length, iteration-statistics and pheromone-update kernels (sm_100a).
+//
+//   k_tour_length      tour_length (model.hpp:205-226) as an int64 warp
+//                      reduction, w_k = 1.0 / (double)C_k
+//                      (inverse_lengths, pheromone.hpp:123-128), and the
+//                      per-city successor/predecessor tables the row-gather
+//                      deposit reads.
+//   k_iter_stats       iteration best (strict <, lowest ant wins ties), the
+//                      int64 length sum for the mean, and the best-so-far tour
+//                      (engine.hpp:117-129, 151-154).
+//   k_evaporate        evaporate (pheromone.hpp:174-189): tau *= (1 - rho),
+//                      one IEEE multiply per cell, 128-bit streaming.
+//   k_deposit_atomic   deposit_accumulate (pheromone.hpp:195-208) as the
+//                      paper's atomic scatter: one thread per (ant, edge),
+//                      two red.global.add.f64.  Order-nondeterministic;
+//                      parity is 1e-5 relative (measured ~1e-16).
+//   k_rows<MODE>       one CTA per pheromone row, fusing
+//                        MODE_GATHER: the deterministic scatter-to-gather
+//                          deposit (gather_cell family, pheromone.hpp:133-341)
+//                          restated in O(m) per row: contributions w_k land in
+//                          a shared-memory row in ascending ant order, then
+//                          tau = fl(fl(tau * keep) + acc)  (bit-exact, :183 then :220);
+//                        MODE_DELTA: tau = fl(fl(tau * keep) + delta) for the
+//                          multi-GPU atomic path (delta all-reduced over NCCL);
+//                      followed (all modes) by compute_choice_info
+//                      (model.hpp:154-173): choice = pow(tau, alpha) *
+//                      eta_beta[dist] with the host-libm table, diagonal 0,
+//                      and the per-row power-of-two scaled fp32 / permuted
+//                      copies the construction kernel streams.
+#pragma once
+
+#include <cstdint>
+
+#include "construct.cuh"
+
+namespace acob200 {
+
+__global__ void k_tour_length(const int32_t* __restrict__ tours, const int32_t* __restrict__ dist,
+                              int n, int P64, int mloc, int64_t* __restrict__ len,
+                              double* __restrict__ inv, int32_t* __restrict__ succ,
+                              int32_t* __restrict__ pred, int S) {
+    const int lane = threadIdx.x & 31;
+    const int warps = blockDim.x >> 5;
+    for (int kl = blockIdx.x * warps + (threadIdx.x >> 5); kl < mloc; kl += gridDim.x * warps) {
+        const int32_t* t = tours + static_cast<size_t>(kl) * (n + 1);
+        long long acc = 0;
+        for (int s = lane; s < n; s += 32) {
+            const int a = t[s], b = t[s + 1];
+            acc += dist[static_cast<size_t>(a) * P64 + b];
+            if (succ) {
+                succ[static_cast<size_t>(a) * S + kl] = b;
+                pred[static_cast<size_t>(b) * S + kl] = a;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);
+        if (lane == 0) {
+            len[kl] = acc;
+            inv[kl] = 1.0 / static_cast<double>(acc);
+        }
+    }
+}
+
+// One CTA.  stats[0] = best length, stats[1] = best local ant, stats[2] =
+// length sum.  Copies the best tour when it strictly improves best_so_far.
+__global__ void __launch_bounds__(1024) k_iter_stats(const int64_t* __restrict__ len, int mloc,
+                                                     const int32_t* __restrict__ tours, int n,
+                                                     long long* __restrict__ stats,
+                                                     long long* __restrict__ best_so_far,
+                                                     int32_t* __restrict__ best_tour,
+                                                     int update_best) {
+    __shared__ long long s_len[32], s_sum[32];
+    __shared__ int s_idx[32];
+    __shared__ int s_improved;
+    long long bl = LLONG_MAX, sum = 0;
+    int bi = INT_MAX;
+    for (int k = threadIdx.x; k < mloc; k += blockDim.x) {
+        const long long l = len[k];
+        sum += l;
+        if (l < bl) { bl = l; bi = k; } // k ascending per thread: first wins
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const long long ol = __shfl_xor_sync(kFull, bl, off);
+        const int oi = __shfl_xor_sync(kFull, bi, off);
+        sum += __shfl_xor_sync(kFull, sum, off);
+        if (ol < bl || (ol == bl && oi < bi)) { bl = ol; bi = oi; }
+    }
+    if (lane == 0) { s_len[w] = bl; s_idx[w] = bi; s_sum[w] = sum; }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        bl = lane < nw ? s_len[lane] : LLONG_MAX;
+        bi = lane < nw ? s_idx[lane] : INT_MAX;
+        sum = lane < nw ? s_sum[lane] : 0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const long long ol = __shfl_xor_sync(kFull, bl, off);
+            const int oi = __shfl_xor_sync(kFull, bi, off);
+            sum += __shfl_xor_sync(kFull, sum, off);
+            if (ol < bl || (ol == bl && oi < bi)) { bl = ol; bi = oi; }
+        }
+        if (lane == 0) {
+            stats[0] = bl;
+            stats[1] = bi;
+            stats[2] = sum;
+            const int imp = update_best && bl < *best_so_far;
+            if (imp) *best_so_far = bl;
+            s_improved = imp;
+        }
+    }
+    __syncthreads();
+    if (s_improved) {
+        const int32_t* src = tours + static_cast<size_t>(s_idx[0]) * (n + 1);
+        for (int s = threadIdx.x; s <= n; s += blockDim.x) best_tour[s] = src[s];
+    }
+}
+
+__global__ void k_evaporate(double* __restrict__ tau, size_t count2, double keep) {
+    double2* t2 = reinterpret_cast<double2*>(tau);
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count2;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        double2 v = t2[i];
+        v.x = __dmul_rn(v.x, keep);
+        v.y = __dmul_rn(v.y, keep);
+        t2[i] = v;
+    }
+}
+
+// One thread per (ant, step); edges (t[s], t[s+1]) and the mirror.
+__global__ void k_deposit_atomic(const int32_t* __restrict__ tours, const double* __restrict__ inv,
+                                 int n, int P64, int mloc, double* __restrict__ target) {
+    const size_t total = static_cast<size_t>(mloc) * n;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int kl = static_cast<int>(i / n), s = static_cast<int>(i - static_cast<size_t>(kl) * n);
+        const int32_t* t = tours + static_cast<size_t>(kl) * (n + 1);
+        const int a = t[s], b = t[s + 1];
+        const double w = inv[kl];
+        atomicAdd(target + static_cast<size_t>(a) * P64 + b, w);
+        atomicAdd(target + static_cast<size_t>(b) * P64 + a, w);
+    }
+}
+
+enum { MODE_CHOICE = 0, MODE_GATHER = 1, MODE_DELTA = 2 };
+
+struct RowParams {
+    double* tau;             // n x P64
+    double* choice64;        // n x P64
+    float* choice32;         // n x PW (fp32 stream) or null
+    double* choice_perm64;   // n x PW (fp64 stream) or null
+    int32_t* scale_exp;      // n
+    const int32_t* dist;     // n x P64
+    const double* lut;       // eta^beta by distance, or null
+    const double* etab;      // n x P64 eta^beta, or null
+    double* delta;           // MODE_DELTA: n x P64
+    const int32_t* succ;     // MODE_GATHER: [shard][city][S]
+    const int32_t* pred;
+    const double* inv;       // [shard][S]
+    int n, P64, PW, C, V;
+    int shards, S, m;        // ants: shard g holds global ants [g*S, min(m,(g+1)*S))
+    double alpha, keep;
+};
+
+__device__ __forceinline__ double tau_pow(double t, double alpha) {
+    if (alpha == 1.0) return t;  // pow(x, 1) == x exactly (SURVEY [E1])
+    if (alpha == 0.0) return 1.0; // pow(x, 0) == 1 exactly
+    return pow(t, alpha);         // parity unpinned for other alpha
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_rows(RowParams p) {
+    extern __shared__ double rowbuf[]; // P64 doubles
+    __shared__ double s_max[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = p.n;
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        double* trow = p.tau + static_cast<size_t>(i) * p.P64;
+        if constexpr (MODE == MODE_GATHER) {
+            for (int j = tid; j < n; j += blockDim.x) rowbuf[j] = 0.0;
+            __syncthreads();
+            // Contributions to column c arrive in ascending global ant order
+            // (shards are contiguous ant ranges); warp `warp` owns columns
+            // c % 8 == warp so its shared-memory updates never race.  Within
+            // a chunk of 16 ants the 32 lanes carry (ant a = lane/2, pred or
+            // succ); equal columns are folded in lane (= ant) order.
+            for (int g = 0; g < p.shards; ++g) {
+                const int kbeg = g * p.S;
+                const int cnt = min(p.S, p.m - kbeg);
+                const int32_t* sc = p.succ + (static_cast<size_t>(g) * n + i) * p.S;
+                const int32_t* pc = p.pred + (static_cast<size_t>(g) * n + i) * p.S;
+                const double* wv = p.inv + static_cast<size_t>(g) * p.S;
+                for (int k0 = 0; k0 < cnt; k0 += 16) {
+                    const int k = k0 + (lane >> 1);
+                    int col = -1;
+                    double w = 0.0;
+                    if (k < cnt) {
+                        col = (lane & 1) ? sc[k] : pc[k];
+                        w = wv[k];
+                    }
+                    const bool mine = col >= 0 && (col & 7) == warp;
+                    const unsigned mm = __ballot_sync(kFull, mine);
+                    if (mine) {
+                        const unsigned grp = __match_any_sync(mm, col);
+                        double acc = rowbuf[col];
+                        for (unsigned b = grp; b; b &= b - 1) acc += __shfl_sync(grp, w, __ffs(b) - 1);
+                        if (lane == __ffs(grp) - 1) rowbuf[col] = acc;
+                    }
+                    __syncwarp();
+                }
+            }
+            __syncthreads();
+        }
+        double mx = 0.0;
+        const int32_t* drow = p.dist + static_cast<size_t>(i) * p.P64;
+        for (int j = tid; j < n; j += blockDim.x) {
+            double t = trow[j];
+            if constexpr (MODE == MODE_GATHER) {
+                t = __dadd_rn(__dmul_rn(t, p.keep), rowbuf[j]);
+                trow[j] = t;
+            } else if constexpr (MODE == MODE_DELTA) {
+                double* drw = p.delta + static_cast<size_t>(i) * p.P64;
+                t = __dadd_rn(__dmul_rn(t, p.keep), drw[j]);
+                drw[j] = 0.0;
+                trow[j] = t;
+            }
+            const double eb = p.etab ? p.etab[static_cast<size_t>(i) * p.P64 + j] : p.lut[drow[j]];
+            const double c = (j == i) ? 0.0 : __dmul_rn(tau_pow(t, p.alpha), eb);
+            p.choice64[static_cast<size_t>(i) * p.P64 + j] = c;
+            rowbuf[j] = c;
+            mx = fmax(mx, c);
+        }
+        if (p.choice32 || p.choice_perm64) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, off));
+            if (lane == 0) s_max[warp] = mx;
+        }
+        __syncthreads();
+        if (p.choice32) {
+            double rmx = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) rmx = fmax(rmx, s_max[w]);
+            // Exact power-of-two scale: row max -> [2^100, 2^101).
+            const int sc = rmx > 0.0 ? 100 - ilogb(rmx) : 0;
+            if (tid == 0) p.scale_exp[i] = sc;
+            float* crow = p.choice32 + static_cast<size_t>(i) * p.PW;
+            for (int q = tid; q < p.PW; q += blockDim.x) {
+                const int c = stream_city(q, p.C, 4);
+                crow[q] = c < n ? __double2float_rn(scalbn(rowbuf[c], sc)) : 0.0f;
+            }
+        }
+        if (p.choice_perm64) {
+            double* crow = p.choice_perm64 + static_cast<size_t>(i) * p.PW;
+            for (int q = tid; q < p.PW; q += blockDim.x) {
+                const int c = stream_city(q, p.C, 2);
+                crow[q] = c < n ? rowbuf[c] : 0.0;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Device Philox self-test (aco_gpu_philox_uniform).
+__global__ void k_philox_test(uint64_t seed, uint32_t it, uint32_t ant, int count,
+                              const uint32_t* steps, const uint32_t* draws, double* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) out[i] = philox_uniform(seed, it, ant, steps[i], draws[i]);
+}
+
+} // namespace acob200

@@ -1,0 +1,214 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Integer outputs (tours, lengths) and the deterministic
+pheromone path must be bit-exact; the atomic path is checked per iteration
+from a shared state within 1e-5 relative (north_star)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ATOMIC_RTOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def aco():
+    from paper_1101_2678_b200 import aco as _aco
+
+    return _aco
+
+
+def make(aco, n, selection=0, deposit=0, stream=0, m=0, ant_range=None, nn=30, seed=1,
+         random_start=False, alpha=1.0, beta=2.0, rho=0.5, spec=None):
+    spec = spec or aco.synthetic_instance(n)
+    prob = aco.build_problem(spec)
+    cfg = aco.RunConfig(params=aco.Parameters(m=m, nn=nn, seed=seed, alpha=alpha, beta=beta,
+                                              rho=rho),
+                        selection=aco.SelectionStrategy(aco.Selection(selection)),
+                        deposit=aco.DepositStrategy(aco.Deposit(deposit)),
+                        stream=aco.WeightStream(stream), random_start=random_start)
+    if ant_range:
+        cfg.ant_begin, cfg.ant_end = ant_range
+    return prob, aco.Engine(prob, cfg)
+
+
+def test_device_philox_matches_oracle(aco, oracle, golden):
+    rows = golden["uniform_at"]
+    for seed, it, ant, st, dr, val in rows[:8]:
+        got = aco.philox_uniform_device(seed, it, ant, [st], [dr])[0]
+        assert got == float(val) == oracle.uniform_at(seed, it, ant, st, dr)
+    rng = np.random.default_rng(3)
+    steps = rng.integers(0, 5000, 4096).astype(np.uint32)
+    draws = rng.integers(0, 5000, 4096).astype(np.uint32)
+    got = aco.philox_uniform_device(1, 7, 123, steps, draws)
+    ref = np.array([oracle.uniform_at(1, 7, 123, int(s), int(d)) for s, d in zip(steps, draws)])
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("n", [198, 1002])
+def test_initial_choice_bit_exact(aco, oracle, n):
+    prob, eng = make(aco, n)
+    with eng:
+        tau = np.full((n, n), eng.tau0)
+        assert eng.tau0 == oracle.tau0(prob.dist, n)
+        assert np.array_equal(eng.choice(), oracle.choice(prob.dist, tau))
+        assert np.array_equal(eng.pheromone(), tau)
+
+
+@pytest.mark.parametrize("stream", [1, 2])
+def test_roulette_iteration0_d198_all_ants(aco, oracle, stream):
+    n = 198
+    prob, eng = make(aco, n, stream=stream)
+    with eng:
+        rec = eng.run_iteration()
+        tau = np.full((n, n), eng.tau0)
+        t_ref, l_ref, _ = oracle.construct(prob.dist, oracle.choice(prob.dist, tau), 1, 0, 0, n)
+        t, l = eng.ants()
+        assert np.array_equal(t, t_ref)
+        assert np.array_equal(l, l_ref)
+        assert rec.best_length == l_ref.min()
+        assert rec.mean_length == l_ref.sum() / n
+
+
+def test_golden_trace_synth198_gather(aco, oracle, golden):
+    """SURVEY App. B trace, reproduced bit-for-bit on the deterministic path."""
+    from pyoracle import fnv1a64
+
+    tr = golden["synth198"]["traces"][1]  # roulette + scatter-gather, 10 iterations
+    assert tr["deposit"] == 1 and tr["selection"] == 0
+    n = 198
+    prob, eng = make(aco, n, deposit=1)
+    with eng:
+        for it in range(10):
+            rec = eng.run_iteration()
+            assert rec.best_length == tr["best"][it]
+            assert repr(rec.mean_length) == tr["mean"][it]
+            t, _ = eng.ants()
+            assert fnv1a64(t) == tr["tours_fnv"][it]
+        assert fnv1a64(eng.pheromone()) == tr["tau_fnv"]
+        assert fnv1a64(eng.choice()) == tr["choice_fnv"]
+        assert eng.best_length() == tr["best_so_far"]
+        assert eng.best_tour().tolist() == tr["best_tour"]
+
+
+def test_golden_trace_synth198_atomic_best_lengths(aco, golden):
+    """Atomic deposit: order-nondeterministic tau (<=1e-15), yet the survey's
+    best-length trace is reproduced (SURVEY [E9])."""
+    tr = golden["synth198"]["traces"][0]
+    prob, eng = make(aco, 198, deposit=0)
+    with eng:
+        best = [eng.run_iteration().best_length for _ in range(10)]
+    assert best == tr["best"]
+
+
+@pytest.mark.parametrize("n,stream", [(1002, 2), (1002, 1)])
+def test_roulette_multi_iteration_gather_bit_exact(aco, oracle, n, stream):
+    prob, eng = make(aco, n, deposit=3, stream=stream)
+    with eng:
+        tau = np.full((n, n), eng.tau0)
+        for it in range(3):
+            ch = oracle.choice(prob.dist, tau)
+            assert np.array_equal(eng.choice(), ch)
+            eng.run_iteration()
+            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, 0, n)
+            t, l = eng.ants()
+            assert np.array_equal(t, t_ref), f"iteration {it}"
+            assert np.array_equal(l, l_ref)
+            tau = oracle.update(tau, t_ref, l_ref, 0.5, 1)
+            assert np.array_equal(eng.pheromone(), tau)
+
+
+def test_atomic_update_within_tolerance_from_shared_state(aco, oracle):
+    n = 1002
+    prob, eng = make(aco, n, deposit=0)
+    with eng:
+        tau = np.full((n, n), eng.tau0)
+        for it in range(3):
+            eng.set_pheromone(tau)
+            ch = oracle.choice(prob.dist, tau)
+            assert np.array_equal(eng.choice(), ch)
+            eng.run_iteration()
+            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, 0, n)
+            t, l = eng.ants()
+            assert np.array_equal(t, t_ref)
+            tau_ref = oracle.update(tau, t_ref, l_ref, 0.5, 0)
+            got = eng.pheromone()
+            rel = np.abs(got - tau_ref) / np.abs(tau_ref)
+            assert rel.max() <= ATOMIC_RTOL
+            tau = tau_ref
+
+
+def test_pr2392_ant_subset_iteration0(aco, oracle, golden):
+    """pr2392 scale: ants 0..15 of iteration 0 against the reference's own
+    golden hash, plus ants 1000..1031 against the oracle."""
+    from pyoracle import fnv1a64
+
+    g = golden["synth2392"]
+    n = 2392
+    for stream in (2, 1):
+        prob, eng = make(aco, n, stream=stream, ant_range=(0, g["ants"]))
+        with eng:
+            eng.construct()
+            t, l = eng.ants()
+            assert fnv1a64(t) == g["roulette_tours_fnv"]
+            assert l.tolist() == g["roulette_lengths"]
+    prob, eng = make(aco, n, ant_range=(1000, 1032))
+    with eng:
+        eng.construct()
+        t, l = eng.ants()
+        tau = np.full((n, n), eng.tau0)
+        t_ref, l_ref, _ = oracle.construct(prob.dist, oracle.choice(prob.dist, tau), 1, 0, 1000,
+                                           1032)
+        assert np.array_equal(t, t_ref)
+
+
+@pytest.mark.parametrize("n", [198, 1002])
+def test_nn_selection_bit_exact(aco, oracle, n):
+    prob, eng = make(aco, n, selection=1, deposit=1)
+    with eng:
+        nnl = oracle.nn_lists(prob.dist, 30)
+        tau = np.full((n, n), eng.tau0)
+        for it in range(3):
+            ch = oracle.choice(prob.dist, tau)
+            eng.run_iteration()
+            t_ref, l_ref, st = oracle.construct(prob.dist, ch, 1, it, 0, n, selection=1,
+                                                nn_lists=nnl)
+            t, l = eng.ants()
+            assert np.array_equal(t, t_ref), f"iteration {it}"
+            tau = oracle.update(tau, t_ref, l_ref, 0.5, 1)
+            assert np.array_equal(eng.pheromone(), tau)
+
+
+def test_data_parallel_selection_bit_exact(aco, oracle):
+    n = 198
+    prob, eng = make(aco, n, selection=2, deposit=1)
+    with eng:
+        tau = np.full((n, n), eng.tau0)
+        for it in range(2):
+            ch = oracle.choice(prob.dist, tau)
+            eng.run_iteration()
+            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, 0, n, selection=2)
+            t, _ = eng.ants()
+            assert np.array_equal(t, t_ref)
+            tau = oracle.update(tau, t_ref, l_ref, 0.5, 1)
+
+
+def test_random_start_bit_exact(aco, oracle):
+    n = 198
+    prob, eng = make(aco, n, random_start=True, deposit=1)
+    with eng:
+        tau = np.full((n, n), eng.tau0)
+        eng.run_iteration()
+        t_ref, _, _ = oracle.construct(prob.dist, oracle.choice(prob.dist, tau), 1, 0, 0, n,
+                                       random_start=True)
+        t, _ = eng.ants()
+        assert np.array_equal(t, t_ref)
+
+
+def test_att48_trace(aco, golden):
+    g = golden["att48"]
+    spec = aco.InstanceSpec("att48", 48, aco.EdgeWeightType.att, np.array(g["xs"]),
+                            np.array(g["ys"]))
+    prob, eng = make(aco, 48, spec=spec, deposit=0)
+    with eng:
+        best = [eng.run_iteration().best_length for _ in range(10)]
+    assert best == g["trace_roulette_accumulate"]["best"]
