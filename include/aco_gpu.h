@@ -172,6 +172,9 @@ aco_status aco_gpu_get_best(aco_gpu_ctx* ctx, int32_t* tour, int64_t* length);
 /* Resolved configuration: m (after m=0 -> n), local ant range, tau0, stream. */
 aco_status aco_gpu_get_info(aco_gpu_ctx* ctx, int32_t* m, int32_t* ant_begin, int32_t* ant_end,
                             double* tau0, int32_t* stream, int32_t* iteration);
+/* The cudaStream_t (as void*) every kernel of this context runs on, so a
+ * caller can time it with CUDA events on the launching stream. */
+void* aco_gpu_stream(aco_gpu_ctx* ctx);
 /* Number of kernel launches issued by this context since creation. */
 int64_t aco_gpu_launch_count(const aco_gpu_ctx* ctx);
 

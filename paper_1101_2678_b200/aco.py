@@ -400,6 +400,10 @@ class Engine:
     def compute_choice_info(self):
         _check(lib.aco_gpu_compute_choice_info(self._h), self._h)
 
+    def stream_handle(self) -> int:
+        """cudaStream_t of this engine (for CUDA-event timing on the launching stream)."""
+        return lib.aco_gpu_stream(self._h)
+
     def launch_count(self) -> int:
         return lib.aco_gpu_launch_count(self._h)
 

@@ -280,11 +280,16 @@ void launch_construct(aco_gpu_ctx* c) {
     if (c->cfg.selection == ACO_SEL_ROULETTE) {
         ConstructFn fn = c->stream_kind == ACO_STREAM_FP64 ? pick_roulette<double>(c->NV, c->MAXR)
                                                            : pick_roulette<float>(c->NV, c->MAXR);
+        const size_t wsz = c->stream_kind == ACO_STREAM_FP64 ? sizeof(double) : sizeof(float);
+        const int ng = (c->NV + 3) / 4;
+        const size_t smem = 128 + static_cast<size_t>(c->PW) * wsz + smem1 +
+                            static_cast<size_t>(c->MAXR) * ng * 32 * wsz;
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem1));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem));
         const int grid = std::max(1, std::min(c->mloc, per_sm * c->num_sms));
         c->construct_grid = grid;
-        fn<<<grid, 32, smem1, c->stream>>>(p);
+        fn<<<grid, 32, smem, c->stream>>>(p);
         check_launch(c, "k_construct_roulette");
     } else if (c->cfg.selection == ACO_SEL_NN) {
         int per_sm = 0;
@@ -679,6 +684,8 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
 const char* aco_gpu_last_error(const aco_gpu_ctx* c) { return c ? c->err.c_str() : g_host_err.c_str(); }
 
 int64_t aco_gpu_launch_count(const aco_gpu_ctx* c) { return c ? c->launches : 0; }
+
+void* aco_gpu_stream(aco_gpu_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
 
 aco_status aco_gpu_set_pheromone(aco_gpu_ctx* c, const double* tau) {
     return guard_ctx(c, [&] {

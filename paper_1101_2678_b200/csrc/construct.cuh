@@ -179,29 +179,83 @@ __device__ __forceinline__ int start_city(const ConstructParams& p, uint32_t kg)
 }
 
 // ---------------------------------------------------------------------------
-// Roulette over the full row.  NV = 128-bit loads per lane per round,
-// C = NV*V cities per lane per round, MAXR = max rounds (R <= MAXR).
+// TMA / mbarrier helpers (cp.async.bulk 1-D copies into shared memory).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Roulette over the full row, one warp (= one CTA) per ant.  Per step:
+//   lane 0 issues one cp.async.bulk of the row (PW * sizeof(WT) bytes) into
+//   shared memory; all lanes draw u (Philox) while it flies; after the
+//   mbarrier completes, lane l reads its contiguous chunk (C cities, NV
+//   conflict-free 128-bit LDS), masks it with its tabu window, tree-sums it in
+//   groups of 4 vectors, and the warp scans the lane sums in fp64.  The chunk
+//   holding the crossing is then re-scanned COOPERATIVELY (EPL elements per
+//   lane, warp scan, ballot) to locate j*, which is certified or replayed.
+// NV = 128-bit vectors per lane per round, C = NV*V, MAXR = max rounds.
 template <typename WT, int NV, int MAXR>
-__global__ void __launch_bounds__(32, 16) k_construct_roulette(ConstructParams p) {
+__global__ void __launch_bounds__(32, MAXR == 1 ? 20 : 12) k_construct_roulette(ConstructParams p) {
     using VT = typename VecOf<WT>::T;
     constexpr int V = VecOf<WT>::V;
     constexpr int C = NV * V;
     constexpr int NWIN = (C + 31) / 32;
-    constexpr int D1 = ceil_log2<C>();
+    constexpr int GV = 4;                              // vectors per tree group
+    constexpr int NG = (NV + GV - 1) / GV;             // groups per chunk
+    constexpr int D1 = ceil_log2<GV * V>() + ceil_log2<NG>();
+    constexpr int GE = GV * V;                         // cities per group
     constexpr bool F32 = sizeof(WT) == 4;
 
-    extern __shared__ uint32_t smem_tabu[];
-    uint32_t* tabu = smem_tabu;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    WT* buf = reinterpret_cast<WT*>(smem_raw + 128);
+    uint32_t* tabu = reinterpret_cast<uint32_t*>(smem_raw + 128 + static_cast<size_t>(p.PW) * sizeof(WT));
+    WT* gsum = reinterpret_cast<WT*>(tabu + p.tabu_words); // [MAXR][NG][32] lane group sums
     const int lane = threadIdx.x & 31;
     const int n = p.n;
     const WT* __restrict__ wbase = static_cast<const WT*>(p.w);
+    const uint32_t row_bytes = static_cast<uint32_t>(p.PW * sizeof(WT));
 
-    // Certification constants (see header comment). All bounds are relative
-    // to an upper bound Thi of the exact (scaled) total.
-    const double rel_ours = (F32 ? (1.0 + D1) * 0x1.0p-24 : D1 * 0x1.0p-53) +
-                            (double)(8 + MAXR + C + 8) * 0x1.0p-53;
-    const double rel_ref = (double)(n + 2) * 0x1.0p-53 * (1.0 + 0x1.0p-30);
-    const double abs_q = F32 ? (double)n * 0x1.0p-149 : 0.0; // 2 * n * 2^-150
+    // Certification constants (header comment); bounds relative to Thi.
+    // e: relative error of every prefix estimate P_j (ours) plus the
+    // reference's own sequential-sum error gamma_n, both relative to the
+    // exact prefix X_j; abs_q: fp32 underflow (2^-150 per element, doubled).
+    const double e_rel = ((F32 ? (1.0 + D1) * 0x1.0p-24 : D1 * 0x1.0p-53) +
+                          (double)(8 + MAXR + NG + 8 + 8) * 0x1.0p-53 +
+                          (double)(n + 2) * 0x1.0p-53) * (1.0 + 0x1.0p-20);
+    const double abs_q = F32 ? (double)n * 0x1.0p-149 : 0.0;
+
+    if (lane == 0) mbar_init(bar, 1);
+    __syncwarp();
+    uint32_t phase = 0;
 
     for (int kl = blockIdx.x; kl < p.mloc; kl += gridDim.x) {
         const uint32_t kg = static_cast<uint32_t>(p.ant_begin + kl);
@@ -213,12 +267,20 @@ __global__ void __launch_bounds__(32, 16) k_construct_roulette(ConstructParams p
             tabu[start >> 5] |= 1u << (start & 31);
             tour[0] = start;
         }
-        __syncwarp();
         int cur = start;
         unsigned long long fb = 0;
 
         for (int step = 1; step < n; ++step) {
-            const WT* __restrict__ row = wbase + static_cast<size_t>(cur) * p.PW;
+            if (lane == 0) {
+                fence_proxy_async_smem(); // generic reads of buf happen-before the refill
+                mbar_expect_tx(bar, row_bytes);
+                tma_row(buf, wbase + static_cast<size_t>(cur) * p.PW, row_bytes, bar);
+            }
+            const double u = philox_uniform(p.seed, p.iteration, kg, static_cast<uint32_t>(step), 0);
+            __syncwarp();
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+
             double incl[MAXR];
             double rtot[MAXR];
             double T = 0.0;
@@ -233,29 +295,36 @@ __global__ void __launch_bounds__(32, 16) k_construct_roulette(ConstructParams p
 #pragma unroll
                     for (int i = 0; i < NWIN; ++i)
                         win[i] = __funnelshift_r(tabu[w0 + i], tabu[w0 + i + 1], sh);
-                    const VT* rv = reinterpret_cast<const VT*>(row + r * 32 * C) + lane;
-                    WT x[C];
+                    const VT* rv = reinterpret_cast<const VT*>(buf + r * 32 * C) + lane;
+                    WT gs[NG];
 #pragma unroll
-                    for (int t = 0; t < NV; ++t) {
-                        const int e0 = t * V;
-                        const uint32_t bits = (win[e0 >> 5] >> (e0 & 31)) & ((1u << V) - 1u);
-                        VT v;
-                        if (bits != (1u << V) - 1u) {
-                            v = __ldg(rv + t * 32);
-                        } else {
-                            if constexpr (F32) v = make_float4(0.f, 0.f, 0.f, 0.f);
-                            else v = make_double2(0.0, 0.0);
+                    for (int g = 0; g < NG; ++g) {
+                        WT x[GV * V];
+#pragma unroll
+                        for (int tt = 0; tt < GV; ++tt) {
+                            const int t = g * GV + tt;
+                            if (t < NV) {
+                                const VT v = rv[t * 32];
+                                if constexpr (F32) {
+                                    x[tt * 4 + 0] = v.x; x[tt * 4 + 1] = v.y;
+                                    x[tt * 4 + 2] = v.z; x[tt * 4 + 3] = v.w;
+                                } else {
+                                    x[tt * 2 + 0] = v.x; x[tt * 2 + 1] = v.y;
+                                }
+                            } else {
+#pragma unroll
+                                for (int q = 0; q < V; ++q) x[tt * V + q] = WT(0);
+                            }
                         }
-                        if constexpr (F32) {
-                            x[e0 + 0] = v.x; x[e0 + 1] = v.y; x[e0 + 2] = v.z; x[e0 + 3] = v.w;
-                        } else {
-                            x[e0 + 0] = v.x; x[e0 + 1] = v.y;
+#pragma unroll
+                        for (int e = 0; e < GV * V; ++e) {
+                            const int ee = g * GV * V + e;
+                            if (ee < C && ((win[ee >> 5] >> (ee & 31)) & 1u)) x[e] = WT(0);
                         }
+                        gs[g] = tree_sum<WT, GV * V>(x);
+                        gsum[(r * NG + g) * 32 + lane] = gs[g];
                     }
-#pragma unroll
-                    for (int e = 0; e < C; ++e)
-                        if ((win[e >> 5] >> (e & 31)) & 1u) x[e] = WT(0);
-                    double d = static_cast<double>(tree_sum<WT, C>(x));
+                    double d = static_cast<double>(tree_sum<WT, NG>(gs));
 #pragma unroll
                     for (int off = 1; off < 32; off <<= 1) {
                         const double y = __shfl_up_sync(kFull, d, off);
@@ -266,12 +335,10 @@ __global__ void __launch_bounds__(32, 16) k_construct_roulette(ConstructParams p
                     T += rtot[r];
                 }
             }
-            const double u = philox_uniform(p.seed, p.iteration, kg, static_cast<uint32_t>(step), 0);
             const double t = u * T;
             bool ok = (T > 0.0) && (T < 1e300);
             int next = -1;
             if (ok) {
-                // round holding the crossing
                 double base = 0.0, my = 0.0;
                 int rs = -1;
 #pragma unroll
@@ -291,48 +358,56 @@ __global__ void __launch_bounds__(32, 16) k_construct_roulette(ConstructParams p
                     ok = false;
                 } else {
                     const int L = __ffs(bal) - 1;
+                    const double start_acc = base + __shfl_sync(kFull, L == 0 ? 0.0 : prev_lane, L);
+                    // 1) group of lane L's chunk holding the crossing: prefix of
+                    //    its NG group sums (broadcast smem reads, fp64)
+                    double gacc = start_acc, gbefore = start_acc;
+                    int G = -1;
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        const double gv = static_cast<double>(gsum[(rs * NG + g) * 32 + L]);
+                        const double na = gacc + gv;
+                        if (G < 0 && na > t) {
+                            G = g;
+                            gbefore = gacc;
+                        }
+                        gacc = na;
+                    }
                     int jstar = -1;
                     double Pj = 0.0, Pprev = 0.0;
-                    if (lane == L) {
-                        double acc = base + (L == 0 ? 0.0 : prev_lane);
+                    if (G >= 0) {
+                        // 2) the GE cities of that group: one per lane, fp64 scan
+                        const int e = G * GE + lane;
                         const int cbase = rs * 32 * C + L * C;
-                        const int w0 = cbase >> 5, sh = cbase & 31;
-                        uint32_t win[NWIN];
+                        double v = 0.0;
+                        if (lane < GE && e < C && !tabu_test(tabu, cbase + e))
+                            v = static_cast<double>(
+                                buf[rs * 32 * C + ((e / V) * 32 + L) * V + (e % V)]);
+                        double pin = v;
 #pragma unroll
-                        for (int i = 0; i < NWIN; ++i)
-                            win[i] = __funnelshift_r(tabu[w0 + i], tabu[w0 + i + 1], sh);
-                        const VT* rv = reinterpret_cast<const VT*>(row + rs * 32 * C) + L;
-#pragma unroll
-                        for (int tt = 0; tt < NV; ++tt) {
-                            const VT v = __ldg(rv + tt * 32);
-                            WT xs[V];
-                            if constexpr (F32) { xs[0] = v.x; xs[1] = v.y; xs[2] = v.z; xs[3] = v.w; }
-                            else { xs[0] = v.x; xs[1] = v.y; }
-#pragma unroll
-                            for (int q = 0; q < V; ++q) {
-                                const int e = tt * V + q;
-                                if (jstar < 0 && !((win[e >> 5] >> (e & 31)) & 1u)) {
-                                    const double na = acc + static_cast<double>(xs[q]);
-                                    if (na > t) {
-                                        jstar = cbase + e;
-                                        Pj = na;
-                                        Pprev = acc;
-                                    }
-                                    acc = na;
-                                }
-                            }
+                        for (int off = 1; off < GE; off <<= 1) {
+                            const double y = __shfl_up_sync(kFull, pin, off);
+                            if (lane >= off) pin += y;
+                        }
+                        const double pup = __shfl_up_sync(kFull, pin, 1);
+                        const unsigned b2 =
+                            __ballot_sync(kFull, lane < GE && v > 0.0 && gbefore + pin > t);
+                        if (b2) {
+                            const int Lw = __ffs(b2) - 1;
+                            jstar = cbase + G * GE + Lw;
+                            Pj = gbefore + __shfl_sync(kFull, pin, Lw);
+                            Pprev = gbefore + (Lw == 0 ? 0.0 : __shfl_sync(kFull, pup, Lw));
                         }
                     }
-                    jstar = __shfl_sync(kFull, jstar, L);
-                    Pj = __shfl_sync(kFull, Pj, L);
-                    Pprev = __shfl_sync(kFull, Pprev, L);
                     if (jstar < 0 || jstar >= n) {
                         ok = false;
                     } else {
+                        // Certification (header comment), margins relative to t:
+                        // |t_ref - t| <= Mt, s_j* >= Pj(1-e) - 2abs, s_prev <= Pprev(1+e) + 2abs.
                         const double Thi = T * (1.0 + 0x1.0p-20) + abs_q;
-                        const double E = (rel_ours + rel_ref + 0x1.0p-51) * Thi + abs_q;
-                        const double M = 2.0 * E * (1.0 + 0x1.0p-20);
-                        ok = (Pj - t > M) && (t - Pprev > M);
+                        const double Mt = (e_rel + 0x1.0p-50) * (u * Thi) + abs_q;
+                        ok = (Pj - e_rel * Pj - 2.0 * abs_q > t + Mt) &&
+                             (Pprev + e_rel * Pprev + 2.0 * abs_q < t - Mt);
                         next = jstar;
                     }
                 }
@@ -342,6 +417,7 @@ __global__ void __launch_bounds__(32, 16) k_construct_roulette(ConstructParams p
                                   p.tabu_words, u, lane);
                 ++fb;
             }
+            __syncwarp();
             if (lane == 0) {
                 tabu[next >> 5] |= 1u << (next & 31);
                 tour[step] = next;

@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(1024) k_iter_stats(const int64_t* __restrict__
                                                      int update_best) {
     __shared__ long long s_len[32], s_sum[32];
     __shared__ int s_idx[32];
-    __shared__ int s_improved;
+    __shared__ int s_improved, s_best;
     long long bl = LLONG_MAX, sum = 0;
     int bi = INT_MAX;
     for (int k = threadIdx.x; k < mloc; k += blockDim.x) {
@@ -108,11 +108,12 @@ __global__ void __launch_bounds__(1024) k_iter_stats(const int64_t* __restrict__
             const int imp = update_best && bl < *best_so_far;
             if (imp) *best_so_far = bl;
             s_improved = imp;
+            s_best = bi;
         }
     }
     __syncthreads();
     if (s_improved) {
-        const int32_t* src = tours + static_cast<size_t>(s_idx[0]) * (n + 1);
+        const int32_t* src = tours + static_cast<size_t>(s_best) * (n + 1);
         for (int s = threadIdx.x; s <= n; s += blockDim.x) best_tour[s] = src[s];
     }
 }

@@ -1,0 +1,120 @@
+"""World-size-2 (gloo, CPU) check of the ant-sharded iteration: the
+decomposition the engine runs over NCCL (paper_1101_2678_b200/sharding.py)
+reproduces the single-process colony — tours identical, gather-path tau
+bit-identical, atomic-path tau within 1e-5, best/mean identical."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n, m, iters, out_path):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from paper_1101_2678_b200.sharding import owner_of, shard_range, shard_size
+    from pyoracle import Oracle, synth_coords
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    O = Oracle.get()
+    xs, ys = synth_coords(n)
+    d = O.build_dist(xs, ys)
+    S = shard_size(m, world)
+    a0, a1 = shard_range(m, world, rank)
+    tau_g = np.full((n, n), O.tau0(d, m))
+    tau_a = tau_g.copy()
+    best_so_far = None
+    trace = []
+    for it in range(iters):
+        # construction of the local shard, global ant ids
+        tg, lg, _ = O.construct(d, O.choice(d, tau_g), 1, it, a0, a1)
+        ta, la, _ = O.construct(d, O.choice(d, tau_a), 1, it, a0, a1)
+        # stats: min len, then min global owner ant among holders, sum
+        loc_best = int(lg.min()) if len(lg) else 2**62
+        t = torch.tensor([loc_best], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        gbest = int(t.item())
+        key = a0 + int(np.argmin(lg)) if loc_best == gbest else 2**62
+        k = torch.tensor([key], dtype=torch.int64)
+        dist.all_reduce(k, op=dist.ReduceOp.MIN)
+        s = torch.tensor([int(lg.sum())], dtype=torch.int64)
+        dist.all_reduce(s, op=dist.ReduceOp.SUM)
+        assert owner_of(int(k.item()), m, world) in range(world)
+        # gather path: all-gather tours (shard-major, padded to S) then fold in order
+        pad = np.full((S, n + 1), -1, np.int32)
+        pad[: a1 - a0] = tg
+        lpad = np.ones(S, np.int64)
+        lpad[: a1 - a0] = lg
+        gt = [torch.zeros((S, n + 1), dtype=torch.int32) for _ in range(world)]
+        gl = [torch.zeros(S, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(gt, torch.from_numpy(pad))
+        dist.all_gather(gl, torch.from_numpy(lpad))
+        tours = np.concatenate([x.numpy() for x in gt])[:m]
+        lens = np.concatenate([x.numpy() for x in gl])[:m]
+        tau_g = O.update(tau_g, tours, lens, 0.5, 1)
+        # atomic path: local delta, all-reduce(sum), tau = tau*keep + delta
+        delta = O.update(np.zeros((n, n)), ta, la, 0.5, 0) if len(la) else np.zeros((n, n))
+        dt = torch.from_numpy(delta)
+        dist.all_reduce(dt, op=dist.ReduceOp.SUM)
+        tau_a = tau_a * 0.5 + dt.numpy()
+        trace.append((gbest, int(k.item()), int(s.item()), tours))
+    if rank == 0:
+        np.savez(out_path, tau_g=tau_g, tau_a=tau_a,
+                 best=np.array([t[0] for t in trace]), owner=np.array([t[1] for t in trace]),
+                 sums=np.array([t[2] for t in trace]), tours=np.stack([t[3] for t in trace]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m", [60, 75])  # 75: uneven shards (38 + 37)
+def test_two_rank_sharded_iteration_equals_single_process(tmp_path, oracle, m):
+    n, iters, world = 60, 3, 2
+    out = str(tmp_path / "r0.npz")
+    mp.spawn(_worker, args=(world, _free_port(), n, m, iters, out), nprocs=world, join=True)
+    got = np.load(out)
+    from pyoracle import synth_coords
+
+    xs, ys = synth_coords(n)
+    d = oracle.build_dist(xs, ys)
+    tau_g = np.full((n, n), oracle.tau0(d, m))
+    tau_a = tau_g.copy()
+    for it in range(iters):
+        t, l, _ = oracle.construct(d, oracle.choice(d, tau_g), 1, it, 0, m)
+        assert np.array_equal(got["tours"][it], t)
+        assert got["best"][it] == l.min()
+        assert got["owner"][it] == int(np.argmin(l))
+        assert got["sums"][it] == l.sum()
+        tau_g = oracle.update(tau_g, t, l, 0.5, 1)
+        ta, la, _ = oracle.construct(d, oracle.choice(d, tau_a), 1, it, 0, m)
+        tau_a = oracle.update(tau_a, ta, la, 0.5, 0)
+    assert np.array_equal(got["tau_g"], tau_g)  # deterministic path: bitwise
+    rel = np.abs(got["tau_a"] - tau_a) / np.abs(tau_a)
+    assert rel.max() <= 1e-5
+
+
+def test_shard_ranges_cover_colony():
+    from paper_1101_2678_b200.sharding import owner_of, shard_range
+
+    for m in (1, 7, 2392, 19136):
+        for world in (1, 2, 3, 4, 8):
+            covered = []
+            for r in range(world):
+                a, b = shard_range(m, world, r)
+                covered.extend(range(a, b))
+                for k in range(a, b):
+                    assert owner_of(k, m, world) == r
+            assert covered == list(range(m))
