@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libaco_gpu.so")
+LIB_PATH = os.environ.get("ACO_GPU_LIB_VARIANT") or os.path.join(HERE, "libaco_gpu.so")
 
 ACO_OK = 0
 ACO_E_CUDA = 100

@@ -117,6 +117,7 @@ struct aco_gpu_ctx {
     long long* d_stats = nullptr;   // [0..2] stats, [3] best_so_far
     int32_t* d_best = nullptr;      // n+1
     unsigned long long* d_fb = nullptr; // [0] roulette fallbacks, [1] nn argmax fallbacks
+    unsigned long long* d_timing = nullptr; // ACO_TIMING phase cycles
     long long* h_stats = nullptr;       // pinned: 4 stats + 2 fallback counters
     ncclComm_t comm = nullptr;
 };
@@ -214,7 +215,7 @@ void choose_stream_layout(aco_gpu_ctx* c) {
     }
     c->C = c->NV * c->V;
     c->PW = c->R * 32 * c->C;
-    c->tabu_words = c->PW / 32 + 4;
+    c->tabu_words = c->PW / 32 + 4; // even, so the fp64 area after it stays 8-byte aligned
 }
 
 void launch_rows(aco_gpu_ctx* c, int mode) {
@@ -270,6 +271,7 @@ ConstructParams make_cp(aco_gpu_ctx* c) {
     p.tabu_words = c->tabu_words;
     p.iteration = static_cast<uint32_t>(c->iteration);
     p.seed = c->seed;
+    p.timing = c->d_timing;
     return p;
 }
 
@@ -283,7 +285,8 @@ void launch_construct(aco_gpu_ctx* c) {
         const size_t wsz = c->stream_kind == ACO_STREAM_FP64 ? sizeof(double) : sizeof(float);
         const int ng = (c->NV + 3) / 4;
         const size_t smem = 128 + static_cast<size_t>(c->PW) * wsz + smem1 +
-                            static_cast<size_t>(c->MAXR) * ng * 32 * wsz;
+                            static_cast<size_t>((c->n + 31) / 32) * sizeof(double) +
+                            (c->MAXR > 1 ? static_cast<size_t>(c->MAXR) * ng * 32 * wsz : 0);
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         int per_sm = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem));
@@ -637,6 +640,10 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         CK(cudaMalloc(&c->d_best, (n + 1) * sizeof(int32_t)));
         CK(cudaMemset(c->d_best, 0, (n + 1) * sizeof(int32_t)));
         CK(cudaMalloc(&c->d_fb, 2 * sizeof(unsigned long long)));
+#if ACO_TIMING
+        CK(cudaMalloc(&c->d_timing, 8 * sizeof(unsigned long long)));
+        CK(cudaMemset(c->d_timing, 0, 8 * sizeof(unsigned long long)));
+#endif
         CK(cudaMallocHost(&c->h_stats, 8 * sizeof(long long)));
 
         if (c->world > 1) {
@@ -667,6 +674,18 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
 
 void aco_gpu_destroy(aco_gpu_ctx* c) {
     if (!c) return;
+#if ACO_TIMING
+    if (c->d_timing) {
+        unsigned long long h[8];
+        cudaMemcpy(h, c->d_timing, sizeof(h), cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "ACO_TIMING cycles per ant-step (all iterations): pass1 %.0f scan %.0f walk %.0f cert %.0f fallback %.0f book %.0f tmawait %.0f\n",
+                     h[0] / (double)c->iteration / c->mloc / (c->n - 1), h[1] / (double)c->iteration / c->mloc / (c->n - 1),
+                     h[2] / (double)c->iteration / c->mloc / (c->n - 1), h[3] / (double)c->iteration / c->mloc / (c->n - 1),
+                     h[4] / (double)c->iteration / c->mloc / (c->n - 1), h[5] / (double)c->iteration / c->mloc / (c->n - 1),
+                     h[6] / (double)c->iteration / c->mloc / (c->n - 1));
+        cudaFree(c->d_timing);
+    }
+#endif
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
     void* bufs[] = {c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,

@@ -37,6 +37,19 @@
 
 #include "philox.cuh"
 
+#ifndef ACO_SCAN32
+#define ACO_SCAN32 0 // lane-sum warp scan in the weight type (fp32) instead of fp64
+#endif
+#ifndef ACO_LDG
+#define ACO_LDG 2 // 1: ld.global.nc.L1::no_allocate; 2: ld.global.nc (L1-allocating)
+#endif
+#ifndef ACO_TIMING
+#define ACO_TIMING 0 // per-phase clock64() accounting into ConstructParams::timing
+#endif
+#ifndef ACO_LANEWALK
+#define ACO_LANEWALK 0 // locate j* inside the crossing chunk with the crossing lane alone
+#endif
+
 namespace acob200 {
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -81,6 +94,7 @@ struct ConstructParams {
     int tabu_words; // per warp; >= PW/32 + 2
     uint32_t iteration;
     uint64_t seed;
+    unsigned long long* timing; // ACO_TIMING: [8] phase cycle totals
 };
 
 __device__ __forceinline__ bool tabu_test(const uint32_t* tabu, int j) {
@@ -107,78 +121,10 @@ __device__ __forceinline__ int lowest_unvisited(const uint32_t* tabu, int words,
 // ascending index order, so all lanes hold the reference's sequential sums.
 // Visited cities contribute +0.0, which leaves a non-negative sum unchanged
 // and can never trigger "acc > target" or last_positive, exactly like the
-// reference's `continue`.
-__device__ __noinline__ int exact_walk(const double* __restrict__ row, const uint32_t* tabu,
-                                       int n, int words, double u, int lane) {
-    double acc = 0.0;
-    double w_next = 0.0;
-    {
-        const int j = lane;
-        if (j < n && !tabu_test(tabu, j)) w_next = row[j];
-    }
-    for (int base = 0; base < n; base += 32) {
-        const double w = w_next;
-        const int j = base + 32 + lane;
-        w_next = (j < n && !tabu_test(tabu, j)) ? row[j] : 0.0;
-#pragma unroll
-        for (int q = 0; q < 32; ++q) acc += __shfl_sync(kFull, w, q);
-    }
-    if (!(acc > 0.0)) return lowest_unvisited(tabu, words, lane); // total <= 0 (:52)
-    const double target = u * acc;                                  // :54
-    double a2 = 0.0;
-    int last_positive = -1;
-    for (int base = 0; base < n; base += 32) {
-        const int j = base + lane;
-        const double w = (j < n && !tabu_test(tabu, j)) ? row[j] : 0.0;
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            const double x = __shfl_sync(kFull, w, q);
-            if (x > 0.0) last_positive = base + q;
-            a2 += x;
-            if (a2 > target) return base + q; // warp-uniform
-        }
-    }
-    if (last_positive >= 0) return last_positive; // :66
-    return lowest_unvisited(tabu, words, lane);
-}
-
-template <typename WT, int C>
-__device__ __forceinline__ WT tree_sum(WT (&x)[C]) {
-#pragma unroll
-    for (int s = 1; s < C; s <<= 1) {
-#pragma unroll
-        for (int i = 0; i + s < C; i += 2 * s) x[i] += x[i + s];
-    }
-    return x[0];
-}
-
-template <int C>
-__host__ __device__ constexpr int ceil_log2() {
-    int d = 0;
-    while ((1 << d) < C) ++d;
-    return d;
-}
-
-__device__ __forceinline__ void tabu_init(uint32_t* tabu, int words, int n, int lane) {
-    for (int wd = lane; wd < words; wd += 32) {
-        const int c0 = wd * 32;
-        uint32_t v;
-        if (c0 + 32 <= n) v = 0u;
-        else if (c0 >= n) v = kFull;
-        else v = kFull << (n - c0);
-        tabu[wd] = v;
-    }
-}
-
-__device__ __forceinline__ int start_city(const ConstructParams& p, uint32_t kg) {
-    if (p.random_start) { // engine.hpp:105-108: burns draw 0 of step 0
-        int s = static_cast<int>(philox_uniform(p.seed, p.iteration, kg, 0, 0) * p.n);
-        return s >= p.n ? p.n - 1 : s;
-    }
-    return static_cast<int>(kg % static_cast<uint32_t>(p.n));
-}
-
-// ---------------------------------------------------------------------------
+// reference's `continue`.  The running sum at every 32-city boundary is kept
+// in `chunk_start` (shared, >= ceil(n/32) doubles), so after the total is
+// known only the crossing chunk is re-folded — from its stored start value,
+// which reproduces the same sequential sums bit for bit.
 // TMA / mbarrier helpers (cp.async.bulk 1-D copies into shared memory).
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -212,46 +158,298 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// The fp64 row is staged through the shared row buffer (`stage`, stage_bytes
+// >= 256) in pieces with TMA, and every lane folds every weight from
+// broadcast shared loads (same address in all lanes), so the only dependence
+// chain is the reference's own sequential fp64 add.
+__device__ __noinline__ int exact_walk(const double* __restrict__ row, const uint32_t* tabu,
+                                       int n, int words, double u, int lane,
+                                       double* chunk_start, double* stage, uint32_t stage_bytes,
+                                       uint64_t* bar, uint32_t& phase) {
+    const int nch = (n + 31) >> 5;
+    const int piece = static_cast<int>(stage_bytes / 256) * 32; // cities per piece (chunk-aligned)
+    double acc = 0.0;
+    int last_positive = -1;
+    for (int p0 = 0; p0 < n; p0 += piece) {
+        const int cnt = min(piece, n - p0);
+        const uint32_t bytes = static_cast<uint32_t>(((cnt * 8) + 15) & ~15);
+        __syncwarp();
+        if (lane == 0) {
+            fence_proxy_async_smem();
+            mbar_expect_tx(bar, bytes);
+            tma_row(stage, row + p0, bytes, bar);
+        }
+        __syncwarp();
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        for (int c = p0 >> 5; c < ((p0 + cnt + 31) >> 5); ++c) {
+            const int base = c << 5;
+            const uint32_t vis = tabu[c];
+            const double2* s2 = reinterpret_cast<const double2*>(stage + (base - p0));
+            if (lane == 0) chunk_start[c] = acc;
+            unsigned pos = 0;
+#pragma unroll
+            for (int q2 = 0; q2 < 16; ++q2) {
+                double2 v = make_double2(0.0, 0.0);
+                if (base + 2 * q2 < n) v = s2[q2];
+                const double x0 = ((vis >> (2 * q2)) & 1u) ? 0.0 : v.x;
+                const double x1 = ((vis >> (2 * q2 + 1)) & 1u) ? 0.0 : v.y;
+                pos |= (x0 > 0.0 ? 1u : 0u) << (2 * q2);
+                pos |= (x1 > 0.0 ? 1u : 0u) << (2 * q2 + 1);
+                acc += x0;
+                acc += x1;
+            }
+            if (pos) last_positive = base + 31 - __clz(pos);
+        }
+    }
+    __syncwarp();
+    if (!(acc > 0.0)) return lowest_unvisited(tabu, words, lane); // total <= 0 (:52)
+    const double target = u * acc;                                  // :54
+    // the crossing lies in the first chunk whose end sum exceeds the target
+    int ch = -1;
+    for (int c0 = 0; c0 < nch && ch < 0; c0 += 32) {
+        const int c = c0 + lane;
+        const double end = c < nch ? (c + 1 < nch ? chunk_start[c + 1] : acc) : -1.0;
+        const unsigned b = __ballot_sync(kFull, c < nch && end > target);
+        if (b) ch = c0 + __ffs(b) - 1;
+    }
+    if (ch < 0) return last_positive >= 0 ? last_positive : lowest_unvisited(tabu, words, lane);
+    // re-fold the crossing chunk from its stored start: lane q keeps the sum
+    // after city base+q (the same sequential adds, so the same values)
+    const int base = ch << 5;
+    const int j = base + lane;
+    const double w = (j < n && !tabu_test(tabu, j)) ? __ldg(row + j) : 0.0;
+    double a2 = chunk_start[ch], mine = 0.0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+        a2 += __shfl_sync(kFull, w, q);
+        mine = (q == lane) ? a2 : mine;
+    }
+    const unsigned cross = __ballot_sync(kFull, mine > target);
+    return base + __ffs(cross) - 1; // first prefix > target (:62)
+}
+
+template <typename WT, int C>
+__device__ __forceinline__ WT tree_sum(WT (&x)[C]) {
+#pragma unroll
+    for (int s = 1; s < C; s <<= 1) {
+#pragma unroll
+        for (int i = 0; i + s < C; i += 2 * s) x[i] += x[i + s];
+    }
+    return x[0];
+}
+
+// Packed (f32x2, sm_100 FADD2) pairwise tree over an even-length group:
+// depth ceil(log2(N)), the same error bound as the scalar tree.
+template <int N>
+__device__ __forceinline__ float tree_sum_packed(float (&x)[N]) {
+    static_assert(N % 2 == 0, "even group");
+    float2 y[N / 2];
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) y[i] = make_float2(x[i], x[N / 2 + i]);
+#pragma unroll
+    for (int s = 1; s < N / 2; s <<= 1) {
+#pragma unroll
+        for (int i = 0; i + s < N / 2; i += 2 * s) y[i] = __fadd2_rn(y[i], y[i + s]);
+    }
+    return y[0].x + y[0].y;
+}
+
+template <int C>
+__host__ __device__ constexpr int ceil_log2() {
+    int d = 0;
+    while ((1 << d) < C) ++d;
+    return d;
+}
+
+__device__ __forceinline__ void tabu_init(uint32_t* tabu, int words, int n, int lane) {
+    for (int wd = lane; wd < words; wd += 32) {
+        const int c0 = wd * 32;
+        uint32_t v;
+        if (c0 + 32 <= n) v = 0u;
+        else if (c0 >= n) v = kFull;
+        else v = kFull << (n - c0);
+        tabu[wd] = v;
+    }
+}
+
+__device__ __forceinline__ int start_city(const ConstructParams& p, uint32_t kg) {
+    if (p.random_start) { // engine.hpp:105-108: burns draw 0 of step 0
+        int s = static_cast<int>(philox_uniform(p.seed, p.iteration, kg, 0, 0) * p.n);
+        return s >= p.n ? p.n - 1 : s;
+    }
+    return static_cast<int>(kg % static_cast<uint32_t>(p.n));
+}
+
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+#if ACO_LDG == 1
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldg(p); }
+
+// ---------------------------------------------------------------------------
+// Middle certification tier: the streamed (fp32) row is still in shared
+// memory; redo every prefix sum in fp64 from it.  The only approximation left
+// is the fp32 quantisation of the weights (2^-24 relative + 2^-150 absolute per
+// city), so the uncertainty band is ~15x narrower than the fp32 pass's.
+// Returns the certified city or -1.
+template <typename WT, int NV, int MAXR>
+__device__ __noinline__ int certify_fp64(const WT* buf, const uint32_t* tabu, int n, int R,
+                                          double u, int lane) {
+    using VT = typename VecOf<WT>::T;
+    constexpr int V = VecOf<WT>::V;
+    constexpr int C = NV * V;
+    constexpr int NWIN = (C + 31) / 32;
+    constexpr bool F32 = sizeof(WT) == 4;
+    const double e_rel = ((F32 ? 2.0 * 0x1.0p-24 : 0.0) +
+                          (double)(2 * C + MAXR + 16) * 0x1.0p-53 +
+                          (double)(n + 8) * 0x1.0p-53) * (1.0 + 0x1.0p-16);
+    const double abs_q = F32 ? (double)n * 0x1.0p-149 : 0.0;
+    double lsum[MAXR];
+    double incl[MAXR];
+    double T = 0.0;
+#pragma unroll
+    for (int r = 0; r < MAXR; ++r) {
+        lsum[r] = 0.0;
+        incl[r] = 0.0;
+        if (r < R) {
+            const int cbase = r * 32 * C + lane * C;
+            const int w0 = cbase >> 5, sh = cbase & 31;
+            uint32_t win[NWIN];
+#pragma unroll
+            for (int i = 0; i < NWIN; ++i) win[i] = __funnelshift_r(tabu[w0 + i], tabu[w0 + i + 1], sh);
+            const VT* rv = reinterpret_cast<const VT*>(buf + r * 32 * C) + lane;
+            double acc = 0.0;
+#pragma unroll
+            for (int tv = 0; tv < NV; ++tv) {
+                const VT v = rv[tv * 32];
+                WT xs[V];
+                if constexpr (F32) { xs[0] = v.x; xs[1] = v.y; xs[2] = v.z; xs[3] = v.w; }
+                else { xs[0] = v.x; xs[1] = v.y; }
+#pragma unroll
+                for (int q = 0; q < V; ++q) {
+                    const int e = tv * V + q;
+                    if (!((win[e >> 5] >> (e & 31)) & 1u)) acc += static_cast<double>(xs[q]);
+                }
+            }
+            lsum[r] = acc;
+            double d = acc;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const double y = __shfl_up_sync(kFull, d, off);
+                if (lane >= off) d += y;
+            }
+            incl[r] = d;
+            T += __shfl_sync(kFull, d, 31);
+        }
+    }
+    if (!(T > 0.0) || !(T < 1e300)) return -1;
+    const double t = u * T;
+    double base = 0.0, my = 0.0, mys = 0.0;
+    int rs = -1;
+#pragma unroll
+    for (int r = 0; r < MAXR; ++r) {
+        if (r < R && rs < 0) {
+            const double rt = __shfl_sync(kFull, incl[r], 31);
+            if (base + rt > t) {
+                rs = r;
+                my = incl[r];
+                mys = lsum[r];
+            } else {
+                base += rt;
+            }
+        }
+    }
+    if (rs < 0) return -1;
+    const unsigned bal = __ballot_sync(kFull, base + my > t);
+    if (!bal) return -1;
+    const int L = __ffs(bal) - 1;
+    int J = -1;
+    bool cert = false;
+    if (lane == L) {
+        double acc = base + (my - mys);
+        const int cbase = rs * 32 * C + L * C;
+        const WT* chunk = buf + rs * 32 * C;
+        for (int e = 0; e < C; ++e) {
+            const int c = cbase + e;
+            if (tabu_test(tabu, c)) continue;
+            const double x = static_cast<double>(chunk[((e / V) * 32 + L) * V + (e % V)]);
+            const double na = acc + x;
+            if (x > 0.0 && na > t) {
+                const double Thi = T * (1.0 + 0x1.0p-16) + abs_q;
+                const double Mt = (e_rel + 0x1.0p-50) * (u * Thi) + abs_q;
+                cert = (na * (1.0 - e_rel) - 2.0 * abs_q > t + Mt) &&
+                       (acc + e_rel * na + 2.0 * abs_q < t - Mt);
+                J = c;
+                break;
+            }
+            acc = na;
+        }
+    }
+    J = __shfl_sync(kFull, J, L);
+    const bool c2 = __shfl_sync(kFull, cert, L);
+    return (c2 && J >= 0 && J < n) ? J : -1;
+}
+
 // ---------------------------------------------------------------------------
 // Roulette over the full row, one warp (= one CTA) per ant.  Per step:
-//   lane 0 issues one cp.async.bulk of the row (PW * sizeof(WT) bytes) into
-//   shared memory; all lanes draw u (Philox) while it flies; after the
-//   mbarrier completes, lane l reads its contiguous chunk (C cities, NV
-//   conflict-free 128-bit LDS), masks it with its tabu window, tree-sums it in
-//   groups of 4 vectors, and the warp scans the lane sums in fp64.  The chunk
-//   holding the crossing is then re-scanned COOPERATIVELY (EPL elements per
-//   lane, warp scan, ballot) to locate j*, which is certified or replayed.
+//   1. the row (PW * sizeof(WT) bytes) is in shared memory: one cp.async.bulk
+//      (TMA) per step, issued SPECULATIVELY for the likely next city as soon
+//      as j* is located, so the L2 latency overlaps certification and
+//      bookkeeping (if certification fails the copy is drained and the true
+//      row fetched);
+//   2. lane l reads its contiguous chunk (NV conflict-free 128-bit LDS),
+//      masks it with its tabu window and tree-sums it in groups of GE cities;
+//      one warp scan of the lane sums gives T and t = u*T;
+//   3. every lane walks its OWN chunk branch-free: group prefix (NG adds) ->
+//      Kogge-Stone prefix of the GE cities of the crossing group -> compare
+//      bitmask -> ffs; each lane certifies its own candidate, so selecting
+//      the result is two ballots and one shuffle.
+// All of 2-3 run in the accumulation type AT: fp32 for the fp32 stream (the
+// fp32 adds on any prefix path are counted in the bound, ~24 * 2^-24), fp64
+// for the fp64 stream.  Only the final two certification compares are fp64.
 // NV = 128-bit vectors per lane per round, C = NV*V, MAXR = max rounds.
 template <typename WT, int NV, int MAXR>
-__global__ void __launch_bounds__(32, MAXR == 1 ? 20 : 12) k_construct_roulette(ConstructParams p) {
+__global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(ConstructParams p) {
     using VT = typename VecOf<WT>::T;
+    using AT = WT; // accumulation type
     constexpr int V = VecOf<WT>::V;
     constexpr int C = NV * V;
     constexpr int NWIN = (C + 31) / 32;
     constexpr int GV = 4;                              // vectors per tree group
     constexpr int NG = (NV + GV - 1) / GV;             // groups per chunk
-    constexpr int D1 = ceil_log2<GV * V>() + ceil_log2<NG>();
     constexpr int GE = GV * V;                         // cities per group
+    constexpr int D1 = ceil_log2<GE>() + ceil_log2<NG>();
     constexpr bool F32 = sizeof(WT) == 4;
+    static_assert(GE <= 32 && 32 % GE == 0, "a group's bits live in one window word");
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
     WT* buf = reinterpret_cast<WT*>(smem_raw + 128);
     uint32_t* tabu = reinterpret_cast<uint32_t*>(smem_raw + 128 + static_cast<size_t>(p.PW) * sizeof(WT));
-    WT* gsum = reinterpret_cast<WT*>(tabu + p.tabu_words); // [MAXR][NG][32] lane group sums
+    double* chunk_start = reinterpret_cast<double*>(tabu + p.tabu_words); // ceil(n/32) (8-aligned)
+    WT* gsum = reinterpret_cast<WT*>(chunk_start + ((p.n + 31) >> 5));   // [MAXR][NG][32]
     const int lane = threadIdx.x & 31;
     const int n = p.n;
     const WT* __restrict__ wbase = static_cast<const WT*>(p.w);
     const uint32_t row_bytes = static_cast<uint32_t>(p.PW * sizeof(WT));
 
-    // Certification constants (header comment); bounds relative to Thi.
-    // e: relative error of every prefix estimate P_j (ours) plus the
-    // reference's own sequential-sum error gamma_n, both relative to the
-    // exact prefix X_j; abs_q: fp32 underflow (2^-150 per element, doubled).
-    const double e_rel = ((F32 ? (1.0 + D1) * 0x1.0p-24 : D1 * 0x1.0p-53) +
-                          (double)(8 + MAXR + NG + 8 + 8) * 0x1.0p-53 +
-                          (double)(n + 2) * 0x1.0p-53) * (1.0 + 0x1.0p-20);
+    // e: bound on |P_j - X_j| / X_j for every prefix estimate (AT adds along
+    // any path: tree D1, warp scan 5, round bases MAXR, group prefix NG,
+    // Kogge-Stone log2 GE, 3 more; + fp32 quantisation of the summands and of
+    // x_j* in Pprev) plus the reference's own sequential error gamma_n.
+    constexpr double ulp_at = F32 ? 0x1.0p-24 : 0x1.0p-53;
+    const double e_rel =
+        ((double)(D1 + 5 + MAXR + NG + 2 + GE / 4 + 4 + 3) * ulp_at +
+         (F32 ? 2.0 * 0x1.0p-24 : 0.0) + (double)(n + 8) * 0x1.0p-53) * (1.0 + 0x1.0p-16);
     const double abs_q = F32 ? (double)n * 0x1.0p-149 : 0.0;
+    const double lo_f = 1.0 - e_rel;
 
     if (lane == 0) mbar_init(bar, 1);
     __syncwarp();
@@ -269,25 +467,42 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 20 : 12) k_construct_roulette(
         }
         int cur = start;
         unsigned long long fb = 0;
+        bool prefetched = false; // row of `cur` already requested by the previous step
+        double ubatch = 0.0;
+#if ACO_TIMING
+        unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        long long tk = clock64();
+#define TICK(i) do { const long long t_ = clock64(); ph[i] += t_ - tk; tk = t_; } while (0)
+#else
+#define TICK(i) do {} while (0)
+#endif
 
         for (int step = 1; step < n; ++step) {
-            if (lane == 0) {
+            if (!prefetched && lane == 0) {
                 fence_proxy_async_smem(); // generic reads of buf happen-before the refill
                 mbar_expect_tx(bar, row_bytes);
                 tma_row(buf, wbase + static_cast<size_t>(cur) * p.PW, row_bytes, bar);
             }
-            const double u = philox_uniform(p.seed, p.iteration, kg, static_cast<uint32_t>(step), 0);
+            // Draw 0 of steps step..step+31: lane i holds step + i (rng.hpp:74-80).
+            if (((step - 1) & 31) == 0)
+                ubatch = philox_uniform(p.seed, p.iteration, kg,
+                                        static_cast<uint32_t>(step + lane), 0);
+            const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
             __syncwarp();
             mbar_wait(bar, phase);
             phase ^= 1u;
+            prefetched = false;
+            TICK(6);
 
-            double incl[MAXR];
-            double rtot[MAXR];
-            double T = 0.0;
+            AT incl[MAXR];
+            AT rtot[MAXR];
+            WT gsr[NG];
+            uint32_t win0[NWIN];
+            AT T = AT(0);
 #pragma unroll
             for (int r = 0; r < MAXR; ++r) {
-                incl[r] = 0.0;
-                rtot[r] = 0.0;
+                incl[r] = AT(0);
+                rtot[r] = AT(0);
                 if (r < p.R) {
                     const int cbase = r * 32 * C + lane * C;
                     const int w0 = cbase >> 5, sh = cbase & 31;
@@ -299,47 +514,64 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 20 : 12) k_construct_roulette(
                     WT gs[NG];
 #pragma unroll
                     for (int g = 0; g < NG; ++g) {
-                        WT x[GV * V];
+                        WT x[GE];
 #pragma unroll
                         for (int tt = 0; tt < GV; ++tt) {
-                            const int t = g * GV + tt;
-                            if (t < NV) {
-                                const VT v = rv[t * 32];
-                                if constexpr (F32) {
-                                    x[tt * 4 + 0] = v.x; x[tt * 4 + 1] = v.y;
-                                    x[tt * 4 + 2] = v.z; x[tt * 4 + 3] = v.w;
-                                } else {
-                                    x[tt * 2 + 0] = v.x; x[tt * 2 + 1] = v.y;
-                                }
+                            const int tv = g * GV + tt;
+                            VT v;
+                            if (tv < NV) {
+                                v = rv[tv * 32];
                             } else {
-#pragma unroll
-                                for (int q = 0; q < V; ++q) x[tt * V + q] = WT(0);
+                                if constexpr (F32) v = make_float4(0.f, 0.f, 0.f, 0.f);
+                                else v = make_double2(0.0, 0.0);
+                            }
+                            if constexpr (F32) {
+                                x[tt * 4 + 0] = v.x; x[tt * 4 + 1] = v.y;
+                                x[tt * 4 + 2] = v.z; x[tt * 4 + 3] = v.w;
+                            } else {
+                                x[tt * 2 + 0] = v.x; x[tt * 2 + 1] = v.y;
                             }
                         }
 #pragma unroll
-                        for (int e = 0; e < GV * V; ++e) {
-                            const int ee = g * GV * V + e;
+                        for (int e = 0; e < GE; ++e) {
+                            const int ee = g * GE + e;
                             if (ee < C && ((win[ee >> 5] >> (ee & 31)) & 1u)) x[e] = WT(0);
                         }
-                        gs[g] = tree_sum<WT, GV * V>(x);
-                        gsum[(r * NG + g) * 32 + lane] = gs[g];
+                        if constexpr (F32) gs[g] = tree_sum_packed<GE>(x);
+                        else gs[g] = tree_sum<WT, GE>(x);
+                        if constexpr (MAXR > 1) gsum[(r * NG + g) * 32 + lane] = gs[g];
                     }
-                    double d = static_cast<double>(tree_sum<WT, NG>(gs));
+                    if constexpr (MAXR == 1) {
+#pragma unroll
+                        for (int g = 0; g < NG; ++g) gsr[g] = gs[g];
+#pragma unroll
+                        for (int i = 0; i < NWIN; ++i) win0[i] = win[i];
+                    }
+                    AT d = static_cast<AT>(tree_sum<WT, NG>(gs));
+                    TICK(0);
 #pragma unroll
                     for (int off = 1; off < 32; off <<= 1) {
-                        const double y = __shfl_up_sync(kFull, d, off);
+                        const AT y = __shfl_up_sync(kFull, d, off);
                         if (lane >= off) d += y;
                     }
                     incl[r] = d;
                     rtot[r] = __shfl_sync(kFull, d, 31);
                     T += rtot[r];
+                    TICK(1);
                 }
             }
-            const double t = u * T;
-            bool ok = (T > 0.0) && (T < 1e300);
+            const double Td = static_cast<double>(T);
+            const double tdd = u * Td;
+            const AT t = static_cast<AT>(tdd); // compare threshold in AT
+            // certification thresholds (T, u only): |t_ref - t| <= Mt
+            const double Thi = Td * (1.0 + 0x1.0p-16) + abs_q;
+            const double Mt = (e_rel + 4.0 * ulp_at) * (u * Thi) + abs_q; // + rounding of t to AT
+            const double A = tdd + Mt + 2.0 * abs_q; // need Pj * (1 - e) > A
+            const double B = tdd - Mt - 2.0 * abs_q; // need Pprev + e * Pj < B
+            bool ok = (T > AT(0)) && (Td < 1e300);
             int next = -1;
             if (ok) {
-                double base = 0.0, my = 0.0;
+                AT base = AT(0), my = AT(0);
                 int rs = -1;
 #pragma unroll
                 for (int r = 0; r < MAXR; ++r) {
@@ -352,71 +584,152 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 20 : 12) k_construct_roulette(
                         }
                     }
                 }
-                const double prev_lane = __shfl_up_sync(kFull, my, 1);
-                const unsigned bal = __ballot_sync(kFull, rs >= 0 && base + my > t);
-                if (bal == 0u) {
-                    ok = false;
-                } else {
-                    const int L = __ffs(bal) - 1;
-                    const double start_acc = base + __shfl_sync(kFull, L == 0 ? 0.0 : prev_lane, L);
-                    // 1) group of lane L's chunk holding the crossing: prefix of
-                    //    its NG group sums (broadcast smem reads, fp64)
-                    double gacc = start_acc, gbefore = start_acc;
+                const AT prev_lane = __shfl_up_sync(kFull, my, 1);
+                int J = -1;        // candidate city of this lane (chunk-relative)
+                bool cert = false; // this lane's candidate certified
+                if (rs >= 0) {
+                    const AT excl = base + (lane == 0 ? AT(0) : prev_lane);
+                    uint32_t win[NWIN];
+                    WT gw[NG];
+                    if constexpr (MAXR == 1) {
+#pragma unroll
+                        for (int i = 0; i < NWIN; ++i) win[i] = win0[i];
+#pragma unroll
+                        for (int g = 0; g < NG; ++g) gw[g] = gsr[g];
+                    } else {
+                        const int cbase = rs * 32 * C + lane * C;
+                        const int w0 = cbase >> 5, sh = cbase & 31;
+#pragma unroll
+                        for (int i = 0; i < NWIN; ++i)
+                            win[i] = __funnelshift_r(tabu[w0 + i], tabu[w0 + i + 1], sh);
+#pragma unroll
+                        for (int g = 0; g < NG; ++g) gw[g] = gsum[(rs * NG + g) * 32 + lane];
+                    }
+                    // group -> quad -> city, each a short sequential prefix with the
+                    // first crossing taken (branch-light selects).
+                    AT acc = excl, gbefore = excl;
                     int G = -1;
 #pragma unroll
                     for (int g = 0; g < NG; ++g) {
-                        const double gv = static_cast<double>(gsum[(rs * NG + g) * 32 + L]);
-                        const double na = gacc + gv;
-                        if (G < 0 && na > t) {
-                            G = g;
-                            gbefore = gacc;
-                        }
-                        gacc = na;
+                        const AT na = acc + static_cast<AT>(gw[g]);
+                        const bool hit = (G < 0) && (na > t);
+                        gbefore = hit ? acc : gbefore;
+                        G = hit ? g : G;
+                        acc = na;
                     }
-                    int jstar = -1;
-                    double Pj = 0.0, Pprev = 0.0;
-                    if (G >= 0) {
-                        // 2) the GE cities of that group: one per lane, fp64 scan
-                        const int e = G * GE + lane;
-                        const int cbase = rs * 32 * C + L * C;
-                        double v = 0.0;
-                        if (lane < GE && e < C && !tabu_test(tabu, cbase + e))
-                            v = static_cast<double>(
-                                buf[rs * 32 * C + ((e / V) * 32 + L) * V + (e % V)]);
-                        double pin = v;
+                    if (G >= 0 && excl <= t) {
+                        uint32_t wsel = win[0];
 #pragma unroll
-                        for (int off = 1; off < GE; off <<= 1) {
-                            const double y = __shfl_up_sync(kFull, pin, off);
-                            if (lane >= off) pin += y;
+                        for (int i = 1; i < NWIN; ++i)
+                            if (((G * GE) >> 5) == i) wsel = win[i];
+                        const uint32_t bits = wsel >> ((G * GE) & 31);
+                        const VT* gv = reinterpret_cast<const VT*>(buf + rs * 32 * C) + lane +
+                                       (G * GV) * 32;
+                        AT y[GE];
+#pragma unroll
+                        for (int tt = 0; tt < GV; ++tt) {
+                            VT v;
+                            if (G * GV + tt < NV) {
+                                v = gv[tt * 32];
+                            } else {
+                                if constexpr (F32) v = make_float4(0.f, 0.f, 0.f, 0.f);
+                                else v = make_double2(0.0, 0.0);
+                            }
+                            if constexpr (F32) {
+                                y[tt * 4 + 0] = v.x; y[tt * 4 + 1] = v.y;
+                                y[tt * 4 + 2] = v.z; y[tt * 4 + 3] = v.w;
+                            } else {
+                                y[tt * 2 + 0] = v.x; y[tt * 2 + 1] = v.y;
+                            }
                         }
-                        const double pup = __shfl_up_sync(kFull, pin, 1);
-                        const unsigned b2 =
-                            __ballot_sync(kFull, lane < GE && v > 0.0 && gbefore + pin > t);
-                        if (b2) {
-                            const int Lw = __ffs(b2) - 1;
-                            jstar = cbase + G * GE + Lw;
-                            Pj = gbefore + __shfl_sync(kFull, pin, Lw);
-                            Pprev = gbefore + (Lw == 0 ? 0.0 : __shfl_sync(kFull, pup, Lw));
+#pragma unroll
+                        for (int q = 0; q < GE; ++q)
+                            if ((bits >> q) & 1u) y[q] = AT(0);
+                        constexpr int NQ = GE / 4; // quads per group
+                        AT qa = gbefore, qbefore = gbefore;
+                        int Q = -1;
+#pragma unroll
+                        for (int k = 0; k < NQ; ++k) {
+                            const AT qs = (y[4 * k] + y[4 * k + 1]) + (y[4 * k + 2] + y[4 * k + 3]);
+                            const AT na = qa + qs;
+                            const bool hit = (Q < 0) && (na > t);
+                            qbefore = hit ? qa : qbefore;
+                            Q = hit ? k : Q;
+                            qa = na;
+                        }
+                        if (Q >= 0) {
+                            AT xs[4];
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) xs[i] = y[i];
+#pragma unroll
+                            for (int k = 1; k < NQ; ++k)
+                                if (k == Q) {
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) xs[i] = y[4 * k + i];
+                                }
+                            AT ea = qbefore, Pj32 = AT(0), Pp32 = AT(0);
+                            int E = -1;
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const AT na = ea + xs[i];
+                                const bool hit = (E < 0) && (xs[i] > AT(0)) && (na > t);
+                                Pj32 = hit ? na : Pj32;
+                                Pp32 = hit ? ea : Pp32;
+                                E = hit ? i : E;
+                                ea = na;
+                            }
+                            if (E >= 0) {
+                                const double Pj = static_cast<double>(Pj32);
+                                const double Pprev = static_cast<double>(Pp32);
+                                J = G * GE + Q * 4 + E;
+                                // both estimates are within e * Pj of their exact prefixes
+                                cert = (Pj * lo_f > A) && (Pprev + e_rel * Pj < B);
+                            }
                         }
                     }
-                    if (jstar < 0 || jstar >= n) {
-                        ok = false;
-                    } else {
-                        // Certification (header comment), margins relative to t:
-                        // |t_ref - t| <= Mt, s_j* >= Pj(1-e) - 2abs, s_prev <= Pprev(1+e) + 2abs.
-                        const double Thi = T * (1.0 + 0x1.0p-20) + abs_q;
-                        const double Mt = (e_rel + 0x1.0p-50) * (u * Thi) + abs_q;
-                        ok = (Pj - e_rel * Pj - 2.0 * abs_q > t + Mt) &&
-                             (Pprev + e_rel * Pprev + 2.0 * abs_q < t - Mt);
+                }
+                TICK(2);
+                const unsigned bal = __ballot_sync(kFull, J >= 0);
+                const unsigned cb = __ballot_sync(kFull, cert);
+                if (bal != 0u) {
+                    const int L = __ffs(bal) - 1;
+                    const int jstar = __shfl_sync(kFull, rs * 32 * C + lane * C + J, L);
+                    ok = ((cb >> L) & 1u) && jstar < n;
+                    if (ok) {
                         next = jstar;
+                        if (step + 1 < n) { // speculative refill: every read of buf in this
+                                            // step has returned (its value fed the ballots)
+                            if (lane == 0) {
+                                mbar_expect_tx(bar, row_bytes);
+                                tma_row(buf, wbase + static_cast<size_t>(jstar) * p.PW, row_bytes, bar);
+                            }
+                            prefetched = true;
+                        }
                     }
+                } else {
+                    ok = false;
+                }
+            }
+            TICK(3);
+            if (!ok) { // middle tier: fp64 sums over the fp32 row still in smem
+                const int j2 = certify_fp64<WT, NV, MAXR>(buf, tabu, n, p.R, u, lane);
+                if (j2 >= 0) {
+                    ok = true;
+                    next = j2;
                 }
             }
             if (!ok) {
+                if (prefetched) { // never set when !ok, kept for safety
+                    mbar_wait(bar, phase);
+                    phase ^= 1u;
+                    prefetched = false;
+                }
                 next = exact_walk(p.w64 + static_cast<size_t>(cur) * p.P64, tabu, n,
-                                  p.tabu_words, u, lane);
+                                  p.tabu_words, u, lane, chunk_start,
+                                  reinterpret_cast<double*>(buf), row_bytes & ~255u, bar, phase);
                 ++fb;
             }
+            TICK(4);
             __syncwarp();
             if (lane == 0) {
                 tabu[next >> 5] |= 1u << (next & 31);
@@ -424,7 +737,13 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 20 : 12) k_construct_roulette(
             }
             __syncwarp();
             cur = next;
+            TICK(5);
         }
+#if ACO_TIMING
+        if (lane == 0 && p.timing)
+            for (int i = 0; i < 7; ++i) atomicAdd(p.timing + i, ph[i]);
+#endif
+#undef TICK
         if (lane == 0) {
             tour[n] = start;
             if (fb) atomicAdd(p.fallbacks, fb);

@@ -57,3 +57,47 @@ extern "C" int aco_probe_read_bw(int device, size_t bytes, int reps, int iters, 
     cudaFree(sink);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
+
+// ---- dependent-chain latency probes (cycles per op, one warp) -------------
+namespace {
+template <int OP>
+__global__ void k_chain(double* out, float* outf, int iters, long long* cyc, double seed) {
+    double d = seed, e = seed * 0.5;
+    float f = static_cast<float>(seed), g = static_cast<float>(seed) * 0.5f;
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            if (OP == 0) d = __dadd_rn(d, e);
+            if (OP == 1) d = __dmul_rn(d, e);
+            if (OP == 2) d = __fma_rn(d, e, e);
+            if (OP == 3) f = __fadd_rn(f, g);
+            if (OP == 4) d = static_cast<double>(static_cast<float>(d) + g);
+            if (OP == 5) d = __shfl_sync(0xffffffffu, d, (threadIdx.x + 1) & 31) + e;
+            if (OP == 6) f = __shfl_sync(0xffffffffu, f, (threadIdx.x + 1) & 31);
+            if (OP == 7) { d = (d > e) ? d - e : d + e; }
+        }
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) *cyc = t1 - t0;
+    out[threadIdx.x] = d;
+    outf[threadIdx.x] = f;
+}
+} // namespace
+
+extern "C" int aco_probe_latency(int device, int op, int iters, double* cycles_per_op) {
+    cudaSetDevice(device);
+    double* out; float* outf; long long* cyc;
+    cudaMalloc(&out, 32 * sizeof(double)); cudaMalloc(&outf, 32 * sizeof(float));
+    cudaMalloc(&cyc, sizeof(long long));
+    void (*fns[])(double*, float*, int, long long*, double) = {k_chain<0>, k_chain<1>, k_chain<2>, k_chain<3>,
+                                                              k_chain<4>, k_chain<5>, k_chain<6>, k_chain<7>};
+    fns[op]<<<1, 32>>>(out, outf, iters, cyc, 1.0000001);
+    cudaDeviceSynchronize();
+    fns[op]<<<1, 32>>>(out, outf, iters, cyc, 1.0000001);
+    long long h = 0;
+    cudaMemcpy(&h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+    *cycles_per_op = static_cast<double>(h) / (16.0 * iters);
+    cudaFree(out); cudaFree(outf); cudaFree(cyc);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}

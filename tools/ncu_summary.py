@@ -16,7 +16,7 @@ import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-        "lts__t_bytes.sum", "lts__t_sectors_op_read.sum", "lts__t_sectors_op_red.sum",
+        "lts__t_sectors.sum", "lts__t_sectors_op_read.sum", "lts__t_sectors_op_red.sum",
         "lts__t_sectors_op_atom.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed",
         "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -67,7 +67,7 @@ def main():
                 u = r["units"]
                 dr = to_bytes(r["dram__bytes_read.sum"], u["dram__bytes_read.sum"])
                 dw = to_bytes(r["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
-                lts = to_bytes(r["lts__t_bytes.sum"], u["lts__t_bytes.sum"])
+                lts = float(str(r["lts__t_sectors.sum"]).replace(",", "")) * 32
                 summary.update({"tag": a.tag, "construct_kernel": r["kernel"],
                                 "construct_dram_bytes_per_launch": int(dr + dw),
                                 "construct_lts_bytes_per_launch": int(lts),
@@ -88,7 +88,7 @@ def main():
         per = collections.defaultdict(list)
         for r in rows[1:]:
             v = float(r[iv].replace(",", ""))
-            v = v / 1e3 if r[iu] == "nsecond" else (v * 1e3 if r[iu] == "msecond" else v)
+            v = v / 1e3 if r[iu] in ("ns", "nsecond") else (v * 1e3 if r[iu] in ("ms", "msecond") else v)
             per[r[ik].split("(")[0]].append(v)  # usecond
         tot = sum(sum(v) for v in per.values())
         share = {k: {"launches": len(v), "total_us": round(sum(v), 1),

@@ -49,6 +49,7 @@ def main():
         print(json.dumps({"it": r.iteration, "best": r.best_length, "construct_ms": round(r.construct_ms, 3),
                           "kernel_ms": round(r.construct_kernel_ms, 3), "update_ms": round(r.update_ms, 3),
                           "choice_ms": round(r.choice_ms, 3), "fallbacks": r.fallbacks}))
+    eng.close()
 
 
 if __name__ == "__main__":
