@@ -108,6 +108,7 @@ struct aco_gpu_ctx {
     double* d_choice_p64 = nullptr;
     int32_t* d_scale = nullptr;
     int32_t* d_nn = nullptr;
+    double* d_choice_nn = nullptr; // n x nn
     int32_t* d_tours = nullptr;
     int64_t* d_len = nullptr;
     double* d_inv = nullptr;   // [world][S]
@@ -232,6 +233,9 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
     rp.succ = c->d_succ;
     rp.pred = c->d_pred;
     rp.inv = c->d_inv;
+    rp.nn_lists = c->d_nn;
+    rp.choice_nn = c->d_choice_nn;
+    rp.nn = c->cfg.nn;
     rp.n = c->n;
     rp.P64 = c->P64;
     rp.PW = c->PW;
@@ -244,6 +248,11 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
     rp.keep = 1.0 - c->cfg.rho; // pheromone.hpp:179
     const size_t smem = static_cast<size_t>(c->P64) * sizeof(double);
     const int grid = std::min(c->n, c->num_sms * 8);
+    if (smem > 48 * 1024) {
+        CK(cudaFuncSetAttribute(k_rows<MODE_CHOICE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k_rows<MODE_GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k_rows<MODE_DELTA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
     if (mode == MODE_CHOICE) k_rows<MODE_CHOICE><<<grid, 256, smem, c->stream>>>(rp);
     else if (mode == MODE_GATHER) k_rows<MODE_GATHER><<<grid, 256, smem, c->stream>>>(rp);
     else k_rows<MODE_DELTA><<<grid, 256, smem, c->stream>>>(rp);
@@ -256,6 +265,7 @@ ConstructParams make_cp(aco_gpu_ctx* c) {
                                             : static_cast<const void*>(c->d_choice32);
     p.w64 = c->d_choice;
     p.nn_lists = c->d_nn;
+    p.choice_nn = c->d_choice_nn;
     p.tours = c->d_tours;
     p.fallbacks = c->d_fb;
     p.argmax_fallbacks = c->d_fb + 1;
@@ -532,6 +542,8 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         c->cfg.beta = prm->beta;
         c->cfg.rho = prm->rho;
         validate(c->cfg);
+        if (c->cfg.selection == ACO_SEL_NN && c->cfg.nn > 64)
+            throw Fail{ACO_E_UNSUPPORTED, "nn lists longer than 64 are not supported"};
         if (c->cfg.m < 1) throw ModelError(Errc::config_error, "ant count must be >= 1");
         c->m = c->cfg.m;
         c->seed = prm->seed;
@@ -620,6 +632,7 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
             CK(cudaMalloc(&c->d_nn, nn_host.size() * sizeof(int32_t)));
             CK(cudaMemcpy(c->d_nn, nn_host.data(), nn_host.size() * sizeof(int32_t),
                           cudaMemcpyHostToDevice));
+            CK(cudaMalloc(&c->d_choice_nn, nn_host.size() * sizeof(double)));
         }
         const size_t ml = std::max(1, c->mloc);
         CK(cudaMalloc(&c->d_tours, ml * (n + 1) * sizeof(int32_t)));
@@ -688,7 +701,7 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
 #endif
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
-    void* bufs[] = {c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
+    void* bufs[] = {c->d_choice_nn, c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
                     c->d_choice_p64, c->d_scale, c->d_nn, c->d_tours, c->d_len, c->d_inv,
                     c->d_succ, c->d_pred, c->d_delta, c->d_stats, c->d_best, c->d_fb};
     for (void* b : bufs)

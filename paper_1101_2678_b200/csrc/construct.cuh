@@ -84,6 +84,7 @@ struct ConstructParams {
     const void* w;           // streamed weights (float or double), row pitch PW
     const double* w64;       // natural fp64 choice, row pitch P64 (exact walk, nn)
     const int32_t* nn_lists; // n x nn (nn selection)
+    const double* choice_nn; // n x nn weights of the nn lists (nn selection)
     int32_t* tours;          // mloc x (n+1)
     unsigned long long* fallbacks;
     unsigned long long* argmax_fallbacks;
@@ -753,12 +754,16 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
 }
 
 // ---------------------------------------------------------------------------
-// NN-list roulette (select_next_nn, construction.hpp:73-121).  The <= nn
-// candidate weights are gathered once (lane q holds list member q) and every
-// lane folds them in LIST order, so the sums are the reference's own: no
-// certification is needed.  When the whole list is visited, the fallback is
-// the exact (value, lowest index) argmax over all unvisited cities
-// (construction.hpp:108-120), which consumes no draw.
+// NN-list roulette (select_next_nn, construction.hpp:73-121).  Lane q holds
+// list member q (nn <= 32 per pass) and its fp64 weight (0 if visited).  One
+// fold over the list: every lane adds the broadcast weights in LIST order —
+// the reference's own sequential sums — and lane q keeps the prefix after
+// member q, so total = last prefix, and the walk's first crossing is one
+// ballot (a visited member adds +0.0 and can never be the first crossing).
+// No certification is needed.  When the whole list is visited, the fallback
+// is the exact (value, lowest index) argmax over all unvisited cities
+// (construction.hpp:108-120), which consumes no draw; it streams the fp64
+// row with 8 independent 16-byte loads per lane in flight.
 __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
     extern __shared__ uint32_t smem_tabu[];
     uint32_t* tabu = smem_tabu;
@@ -777,33 +782,25 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
         __syncwarp();
         int cur = start;
         unsigned long long fb = 0;
+        double ubatch = 0.0;
         for (int step = 1; step < n; ++step) {
             const double* __restrict__ row = p.w64 + static_cast<size_t>(cur) * p.P64;
             const int32_t* nb = p.nn_lists + static_cast<size_t>(cur) * nn;
+            const double* wn = p.choice_nn + static_cast<size_t>(cur) * nn;
+            if (((step - 1) & 31) == 0)
+                ubatch = philox_uniform(p.seed, p.iteration, kg,
+                                        static_cast<uint32_t>(step + lane), 0);
+            const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
             int next = -1;
-            bool any = false;
-            // candidates in chunks of 32 list members (nn is usually <= 32)
-            double total = 0.0;
-            for (int q0 = 0; q0 < nn; q0 += 32) {
-                const int q = q0 + lane;
-                int j = -1;
-                double w = 0.0;
-                bool un = false;
-                if (q < nn) {
-                    j = nb[q];
-                    un = !tabu_test(tabu, j);
-                    if (un) w = row[j];
-                }
-                any |= (__ballot_sync(kFull, un) != 0u);
-                const int cnt = min(32, nn - q0);
-                for (int s = 0; s < cnt; ++s) total += __shfl_sync(kFull, w, s);
-            }
-            if (any) {
-                const double u = philox_uniform(p.seed, p.iteration, kg, static_cast<uint32_t>(step), 0);
-                int first_un = -1, last_positive = -1;
-                const double target = u * total;
-                double acc = 0.0;
-                for (int q0 = 0; q0 < nn && next < 0; q0 += 32) {
+            // fold: lane q of pass k holds member 32k+q
+            double acc = 0.0;
+            int first_un = -1, last_pos = -1;
+            double mine[2] = {0.0, 0.0};
+            int jm[2] = {-1, -1};
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int q0 = 32 * k;
+                if (q0 < nn) {
                     const int q = q0 + lane;
                     int j = -1;
                     double w = 0.0;
@@ -811,31 +808,81 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
                     if (q < nn) {
                         j = nb[q];
                         un = !tabu_test(tabu, j);
-                        if (un) w = row[j];
+                        if (un) w = wn[q];
                     }
+                    jm[k] = j;
                     const unsigned unb = __ballot_sync(kFull, un);
+                    const unsigned pob = __ballot_sync(kFull, un && w > 0.0);
                     if (first_un < 0 && unb) first_un = __shfl_sync(kFull, j, __ffs(unb) - 1);
-                    const int cnt = min(32, nn - q0);
-                    for (int s = 0; s < cnt; ++s) {
-                        const double x = __shfl_sync(kFull, w, s);
-                        const int js = __shfl_sync(kFull, j, s);
-                        if (next < 0 && ((unb >> s) & 1u)) {
-                            if (x > 0.0) last_positive = js;
-                            acc += x;
-                            if (total > 0.0 && acc > target) next = js;
-                        }
+                    if (pob) last_pos = __shfl_sync(kFull, j, 31 - __clz(pob));
+                    // lanes >= nn carry w = +0.0, so folding all 32 is exact
+                    double wq[32];
+#pragma unroll
+                    for (int s2 = 0; s2 < 32; ++s2) wq[s2] = __shfl_sync(kFull, w, s2);
+#pragma unroll
+                    for (int s2 = 0; s2 < 32; ++s2) {
+                        acc += wq[s2];
+                        mine[k] = (s2 == lane) ? acc : mine[k];
                     }
                 }
-                if (!(total > 0.0)) next = first_un;                 // :89-92
-                else if (next < 0) next = last_positive >= 0 ? last_positive : first_un; // :103-105
+            }
+            if (first_un >= 0) {
+                const double total = acc;
+                if (!(total > 0.0)) {
+                    next = first_un;                                     // :89-92
+                } else {
+                    const double target = u * total;                     // :93
+#pragma unroll
+                    for (int k = 0; k < 2 && next < 0; ++k) {
+                        if (32 * k < nn) {
+                            const unsigned cr = __ballot_sync(kFull, lane + 32 * k < nn && mine[k] > target);
+                            if (cr) next = __shfl_sync(kFull, jm[k], __ffs(cr) - 1);
+                        }
+                    }
+                    if (next < 0) next = last_pos >= 0 ? last_pos : first_un; // :103-105
+                }
             } else {
                 // argmax over all unvisited, lowest index on ties (:108-120)
                 double bw = -1.0;
                 int bj = -1;
-                for (int j = lane; j < n; j += 32) {
-                    if (!tabu_test(tabu, j)) {
-                        const double w = row[j];
-                        if (w > bw) { bw = w; bj = j; }
+                const double2* r2 = reinterpret_cast<const double2*>(row);
+                const int n2 = (n + 1) >> 1;
+                if (4 * (n - step) < n) {
+                    // few cities left: gather only the unvisited ones (8 in flight)
+                    for (int w0 = 0; w0 < p.tabu_words; w0 += 32) {
+                        const int wd = w0 + lane;
+                        uint32_t freeb = wd < p.tabu_words ? ~tabu[wd] : 0u;
+                        while (freeb) {
+                            int js[8];
+                            double vs[8];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                js[i] = -1;
+                                if (freeb) {
+                                    js[i] = wd * 32 + __ffs(freeb) - 1;
+                                    freeb &= freeb - 1;
+                                }
+                            }
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) vs[i] = js[i] >= 0 ? __ldg(row + js[i]) : -1.0;
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                if (js[i] >= 0 && vs[i] > bw) { bw = vs[i]; bj = js[i]; }
+                        }
+                    }
+                } else
+                for (int b0 = 0; b0 < n2; b0 += 32 * 8) {
+                    double2 v[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int k2 = b0 + i * 32 + lane;
+                        v[i] = k2 < n2 ? __ldg(r2 + k2) : make_double2(-1.0, -1.0);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int j0 = 2 * (b0 + i * 32 + lane);
+                        if (j0 < n && !tabu_test(tabu, j0) && v[i].x > bw) { bw = v[i].x; bj = j0; }
+                        if (j0 + 1 < n && !tabu_test(tabu, j0 + 1) && v[i].y > bw) { bw = v[i].y; bj = j0 + 1; }
                     }
                 }
 #pragma unroll

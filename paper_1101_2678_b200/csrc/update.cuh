@@ -159,6 +159,9 @@ struct RowParams {
     const int32_t* succ;     // MODE_GATHER: [shard][city][S]
     const int32_t* pred;
     const double* inv;       // [shard][S]
+    const int32_t* nn_lists; // n x nn (nn selection) or null
+    double* choice_nn;       // n x nn: choice64[i][nn_lists[i][q]] (nn selection)
+    int nn;
     int n, P64, PW, C, V;
     int shards, S, m;        // ants: shard g holds global ants [g*S, min(m,(g+1)*S))
     double alpha, keep;
@@ -238,6 +241,11 @@ __global__ void __launch_bounds__(256) k_rows(RowParams p) {
             if (lane == 0) s_max[warp] = mx;
         }
         __syncthreads();
+        if (p.choice_nn) { // the nn list's weights, contiguous per row (L2-resident)
+            for (int q = tid; q < p.nn; q += blockDim.x)
+                p.choice_nn[static_cast<size_t>(i) * p.nn + q] =
+                    rowbuf[p.nn_lists[static_cast<size_t>(i) * p.nn + q]];
+        }
         if (p.choice32) {
             double rmx = 0.0;
             for (int w = 0; w < (int)(blockDim.x >> 5); ++w) rmx = fmax(rmx, s_max[w]);
