@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
     // x_j* in Pprev) plus the reference's own sequential error gamma_n.
     constexpr double ulp_at = F32 ? 0x1.0p-24 : 0x1.0p-53;
     const double e_rel =
-        ((double)(D1 + 5 + MAXR + NG + 2 + GE / 4 + 4 + 3) * ulp_at +
+        ((double)(D1 + 5 + MAXR + 1 + 2 + 5 + 4 + 3) * ulp_at +
          (F32 ? 2.0 * 0x1.0p-24 : 0.0) + (double)(n + 8) * 0x1.0p-53) * (1.0 + 0x1.0p-16);
     const double abs_q = F32 ? (double)n * 0x1.0p-149 : 0.0;
     const double lo_f = 1.0 - e_rel;
@@ -585,130 +585,84 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                         }
                     }
                 }
-                const AT prev_lane = __shfl_up_sync(kFull, my, 1);
-                int J = -1;        // candidate city of this lane (chunk-relative)
-                bool cert = false; // this lane's candidate certified
-                if (rs >= 0) {
-                    const AT excl = base + (lane == 0 ? AT(0) : prev_lane);
-                    uint32_t win[NWIN];
-                    WT gw[NG];
-                    if constexpr (MAXR == 1) {
-#pragma unroll
-                        for (int i = 0; i < NWIN; ++i) win[i] = win0[i];
-#pragma unroll
-                        for (int g = 0; g < NG; ++g) gw[g] = gsr[g];
-                    } else {
-                        const int cbase = rs * 32 * C + lane * C;
-                        const int w0 = cbase >> 5, sh = cbase & 31;
-#pragma unroll
-                        for (int i = 0; i < NWIN; ++i)
-                            win[i] = __funnelshift_r(tabu[w0 + i], tabu[w0 + i + 1], sh);
-#pragma unroll
-                        for (int g = 0; g < NG; ++g) gw[g] = gsum[(rs * NG + g) * 32 + lane];
-                    }
-                    // group -> quad -> city, each a short sequential prefix with the
-                    // first crossing taken (branch-light selects).
-                    AT acc = excl, gbefore = excl;
-                    int G = -1;
-#pragma unroll
-                    for (int g = 0; g < NG; ++g) {
-                        const AT na = acc + static_cast<AT>(gw[g]);
-                        const bool hit = (G < 0) && (na > t);
-                        gbefore = hit ? acc : gbefore;
-                        G = hit ? g : G;
-                        acc = na;
-                    }
-                    if (G >= 0 && excl <= t) {
-                        uint32_t wsel = win[0];
-#pragma unroll
-                        for (int i = 1; i < NWIN; ++i)
-                            if (((G * GE) >> 5) == i) wsel = win[i];
-                        const uint32_t bits = wsel >> ((G * GE) & 31);
-                        const VT* gv = reinterpret_cast<const VT*>(buf + rs * 32 * C) + lane +
-                                       (G * GV) * 32;
-                        AT y[GE];
-#pragma unroll
-                        for (int tt = 0; tt < GV; ++tt) {
-                            VT v;
-                            if (G * GV + tt < NV) {
-                                v = gv[tt * 32];
-                            } else {
-                                if constexpr (F32) v = make_float4(0.f, 0.f, 0.f, 0.f);
-                                else v = make_double2(0.0, 0.0);
-                            }
-                            if constexpr (F32) {
-                                y[tt * 4 + 0] = v.x; y[tt * 4 + 1] = v.y;
-                                y[tt * 4 + 2] = v.z; y[tt * 4 + 3] = v.w;
-                            } else {
-                                y[tt * 2 + 0] = v.x; y[tt * 2 + 1] = v.y;
-                            }
+                // crossing lane L of round rs, then a cooperative walk over L's
+                // chunk: lane k takes quad k (4 consecutive cities), quad sums are
+                // scanned across the warp, and the lane holding the crossing quad
+                // walks its 4 cities.
+                const unsigned lb = __ballot_sync(kFull, rs >= 0 && base + my > t);
+                int J = -1;        // candidate city (global index), valid in lane Q
+                bool cert = false; // its certification
+                int Q = -1;
+                if (lb) {
+                    const int L = __ffs(lb) - 1;
+                    const AT myprev = __shfl_sync(kFull, my, L == 0 ? 0 : L - 1);
+                    const AT exclL = base + (L == 0 ? AT(0) : myprev);
+                    constexpr int NQT = C / 4; // quads per chunk
+                    const int cbaseL = rs * 32 * C + L * C;
+                    AT xv[4] = {AT(0), AT(0), AT(0), AT(0)};
+                    if (lane < NQT) {
+                        const int e0 = 4 * lane;
+                        if constexpr (F32) {
+                            const float4 v = *reinterpret_cast<const float4*>(
+                                buf + rs * 32 * C + (lane * 32 + L) * 4);
+                            xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
+                        } else {
+                            const double2 v0 = *reinterpret_cast<const double2*>(
+                                buf + rs * 32 * C + ((2 * lane) * 32 + L) * 2);
+                            const double2 v1 = *reinterpret_cast<const double2*>(
+                                buf + rs * 32 * C + ((2 * lane + 1) * 32 + L) * 2);
+                            xv[0] = v0.x; xv[1] = v0.y; xv[2] = v1.x; xv[3] = v1.y;
                         }
+                        const int c0 = cbaseL + e0;
+                        const uint32_t bits4 =
+                            __funnelshift_r(tabu[c0 >> 5], tabu[(c0 >> 5) + 1], c0 & 31);
 #pragma unroll
-                        for (int q = 0; q < GE; ++q)
-                            if ((bits >> q) & 1u) y[q] = AT(0);
-                        constexpr int NQ = GE / 4; // quads per group
-                        AT qa = gbefore, qbefore = gbefore;
-                        int Q = -1;
+                        for (int q = 0; q < 4; ++q)
+                            if ((bits4 >> q) & 1u) xv[q] = AT(0);
+                    }
+                    const AT qs = (xv[0] + xv[1]) + (xv[2] + xv[3]);
+                    AT qi = qs;
 #pragma unroll
-                        for (int k = 0; k < NQ; ++k) {
-                            const AT qs = (y[4 * k] + y[4 * k + 1]) + (y[4 * k + 2] + y[4 * k + 3]);
-                            const AT na = qa + qs;
-                            const bool hit = (Q < 0) && (na > t);
-                            qbefore = hit ? qa : qbefore;
-                            Q = hit ? k : Q;
-                            qa = na;
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const AT y = __shfl_up_sync(kFull, qi, off);
+                        if (lane >= off) qi += y;
+                    }
+                    const AT qe = __shfl_up_sync(kFull, qi, 1);
+                    const unsigned qb = __ballot_sync(kFull, lane < NQT && exclL + qi > t);
+                    Q = __ffs(qb) - 1;
+                    if (lane == Q) {
+                        AT ea = exclL + (lane == 0 ? AT(0) : qe);
+                        AT Pj32 = AT(0), Pp32 = AT(0);
+                        int E = -1;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const AT na = ea + xv[q];
+                            const bool hit = (E < 0) && (xv[q] > AT(0)) && (na > t);
+                            Pj32 = hit ? na : Pj32;
+                            Pp32 = hit ? ea : Pp32;
+                            E = hit ? q : E;
+                            ea = na;
                         }
-                        if (Q >= 0) {
-                            AT xs[4];
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) xs[i] = y[i];
-#pragma unroll
-                            for (int k = 1; k < NQ; ++k)
-                                if (k == Q) {
-#pragma unroll
-                                    for (int i = 0; i < 4; ++i) xs[i] = y[4 * k + i];
-                                }
-                            AT ea = qbefore, Pj32 = AT(0), Pp32 = AT(0);
-                            int E = -1;
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const AT na = ea + xs[i];
-                                const bool hit = (E < 0) && (xs[i] > AT(0)) && (na > t);
-                                Pj32 = hit ? na : Pj32;
-                                Pp32 = hit ? ea : Pp32;
-                                E = hit ? i : E;
-                                ea = na;
-                            }
-                            if (E >= 0) {
-                                const double Pj = static_cast<double>(Pj32);
-                                const double Pprev = static_cast<double>(Pp32);
-                                J = G * GE + Q * 4 + E;
-                                // both estimates are within e * Pj of their exact prefixes
-                                cert = (Pj * lo_f > A) && (Pprev + e_rel * Pj < B);
-                            }
+                        if (E >= 0) {
+                            J = cbaseL + 4 * lane + E;
+                            const double Pj = static_cast<double>(Pj32);
+                            const double Pprev = static_cast<double>(Pp32);
+                            cert = (Pj * lo_f > A) && (Pprev + e_rel * Pj < B) && J < n;
                         }
                     }
                 }
                 TICK(2);
-                const unsigned bal = __ballot_sync(kFull, J >= 0);
+                // speculative refill, issued by the certifying lane itself: every
+                // read of buf in this step has returned (its value fed the ballots)
+                if (cert && step + 1 < n) {
+                    mbar_expect_tx(bar, row_bytes);
+                    tma_row(buf, wbase + static_cast<size_t>(J) * p.PW, row_bytes, bar);
+                }
                 const unsigned cb = __ballot_sync(kFull, cert);
-                if (bal != 0u) {
-                    const int L = __ffs(bal) - 1;
-                    const int jstar = __shfl_sync(kFull, rs * 32 * C + lane * C + J, L);
-                    ok = ((cb >> L) & 1u) && jstar < n;
-                    if (ok) {
-                        next = jstar;
-                        if (step + 1 < n) { // speculative refill: every read of buf in this
-                                            // step has returned (its value fed the ballots)
-                            if (lane == 0) {
-                                mbar_expect_tx(bar, row_bytes);
-                                tma_row(buf, wbase + static_cast<size_t>(jstar) * p.PW, row_bytes, bar);
-                            }
-                            prefetched = true;
-                        }
-                    }
-                } else {
-                    ok = false;
+                ok = cb != 0u;
+                if (ok) {
+                    next = __shfl_sync(kFull, J, __ffs(cb) - 1);
+                    prefetched = step + 1 < n;
                 }
             }
             TICK(3);
@@ -731,12 +685,14 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                 ++fb;
             }
             TICK(4);
-            __syncwarp();
+            // Every read of the shared tabu in this step has been consumed by a
+            // ballot/shuffle, so lane 0 updates it without a barrier; the
+            // __syncwarp before the next step's mbarrier wait orders it before
+            // any later read.
             if (lane == 0) {
                 tabu[next >> 5] |= 1u << (next & 31);
                 tour[step] = next;
             }
-            __syncwarp();
             cur = next;
             TICK(5);
         }
