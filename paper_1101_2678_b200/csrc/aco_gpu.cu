@@ -215,8 +215,8 @@ void choose_stream_layout(aco_gpu_ctx* c) {
                                               " with this weight stream"};
     }
     c->C = c->NV * c->V;
-    c->PW = c->R * 32 * c->C;
-    c->tabu_words = c->PW / 32 + 4; // even, so the fp64 area after it stays 8-byte aligned
+    c->PW = c->R * kLP * c->C;        // physical row length (with pad slots)
+    c->tabu_words = c->R * c->C + 4;  // covers R*32*C cities; even, keeps the fp64 area 8-aligned
 }
 
 void launch_rows(aco_gpu_ctx* c, int mode) {

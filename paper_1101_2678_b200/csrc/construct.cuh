@@ -64,20 +64,28 @@ template <> struct VecOf<double> {
     static constexpr int V = 2;
 };
 
+// Physical layout of a streamed row: LP = 33 vector slots per line (32 lanes
+// + 1 pad slot) so that a warp reading one lane's chunk (the crossing walk)
+// spreads over 8 bank groups instead of one.  Round r holds cities
+// [r*32C, (r+1)*32C) in LP*C elements.
+constexpr int kLP = 33;
+
 __host__ __device__ __forceinline__ int stream_pos(int c, int C, int V) {
     const int R32 = 32 * C;
     const int r = c / R32, rem = c - r * R32;
     const int l = rem / C, e = rem - l * C;
     const int t = e / V, q = e - t * V;
-    return r * R32 + (t * 32 + l) * V + q;
+    return r * (kLP * C) + (t * kLP + l) * V + q;
 }
 
+// Inverse of stream_pos; returns INT_MAX for pad slots.
 __host__ __device__ __forceinline__ int stream_city(int p, int C, int V) {
-    const int R32 = 32 * C;
-    const int r = p / R32, rem = p - r * R32;
-    const int t = rem / (32 * V), rem2 = rem - t * 32 * V;
+    const int RS = kLP * C;
+    const int r = p / RS, rem = p - r * RS;
+    const int t = rem / (kLP * V), rem2 = rem - t * kLP * V;
     const int l = rem2 / V, q = rem2 - l * V;
-    return r * R32 + l * C + t * V + q;
+    if (l >= 32) return 0x7fffffff;
+    return r * 32 * C + l * C + t * V + q;
 }
 
 struct ConstructParams {
@@ -325,11 +333,11 @@ __device__ __noinline__ int certify_fp64(const WT* buf, const uint32_t* tabu, in
             uint32_t win[NWIN];
 #pragma unroll
             for (int i = 0; i < NWIN; ++i) win[i] = __funnelshift_r(tabu[w0 + i], tabu[w0 + i + 1], sh);
-            const VT* rv = reinterpret_cast<const VT*>(buf + r * 32 * C) + lane;
+            const VT* rv = reinterpret_cast<const VT*>(buf + r * kLP * C) + lane;
             double acc = 0.0;
 #pragma unroll
             for (int tv = 0; tv < NV; ++tv) {
-                const VT v = rv[tv * 32];
+                const VT v = rv[tv * kLP];
                 WT xs[V];
                 if constexpr (F32) { xs[0] = v.x; xs[1] = v.y; xs[2] = v.z; xs[3] = v.w; }
                 else { xs[0] = v.x; xs[1] = v.y; }
@@ -376,11 +384,11 @@ __device__ __noinline__ int certify_fp64(const WT* buf, const uint32_t* tabu, in
     if (lane == L) {
         double acc = base + (my - mys);
         const int cbase = rs * 32 * C + L * C;
-        const WT* chunk = buf + rs * 32 * C;
+        const WT* chunk = buf + rs * kLP * C;
         for (int e = 0; e < C; ++e) {
             const int c = cbase + e;
             if (tabu_test(tabu, c)) continue;
-            const double x = static_cast<double>(chunk[((e / V) * 32 + L) * V + (e % V)]);
+            const double x = static_cast<double>(chunk[((e / V) * kLP + L) * V + (e % V)]);
             const double na = acc + x;
             if (x > 0.0 && na > t) {
                 const double Thi = T * (1.0 + 0x1.0p-16) + abs_q;
@@ -511,7 +519,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
 #pragma unroll
                     for (int i = 0; i < NWIN; ++i)
                         win[i] = __funnelshift_r(tabu[w0 + i], tabu[w0 + i + 1], sh);
-                    const VT* rv = reinterpret_cast<const VT*>(buf + r * 32 * C) + lane;
+                    const VT* rv = reinterpret_cast<const VT*>(buf + r * kLP * C) + lane;
                     WT gs[NG];
 #pragma unroll
                     for (int g = 0; g < NG; ++g) {
@@ -521,7 +529,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                             const int tv = g * GV + tt;
                             VT v;
                             if (tv < NV) {
-                                v = rv[tv * 32];
+                                v = rv[tv * kLP];
                             } else {
                                 if constexpr (F32) v = make_float4(0.f, 0.f, 0.f, 0.f);
                                 else v = make_double2(0.0, 0.0);
@@ -604,13 +612,13 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                         const int e0 = 4 * lane;
                         if constexpr (F32) {
                             const float4 v = *reinterpret_cast<const float4*>(
-                                buf + rs * 32 * C + (lane * 32 + L) * 4);
+                                buf + rs * kLP * C + (lane * kLP + L) * 4);
                             xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
                         } else {
                             const double2 v0 = *reinterpret_cast<const double2*>(
-                                buf + rs * 32 * C + ((2 * lane) * 32 + L) * 2);
+                                buf + rs * kLP * C + ((2 * lane) * kLP + L) * 2);
                             const double2 v1 = *reinterpret_cast<const double2*>(
-                                buf + rs * 32 * C + ((2 * lane + 1) * 32 + L) * 2);
+                                buf + rs * kLP * C + ((2 * lane + 1) * kLP + L) * 2);
                             xv[0] = v0.x; xv[1] = v0.y; xv[2] = v1.x; xv[3] = v1.y;
                         }
                         const int c0 = cbaseL + e0;

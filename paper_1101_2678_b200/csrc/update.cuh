@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(256) k_rows(RowParams p) {
             float* crow = p.choice32 + static_cast<size_t>(i) * p.PW;
             for (int q = tid; q < p.PW; q += blockDim.x) {
                 const int c = stream_city(q, p.C, 4);
-                crow[q] = c < n ? __double2float_rn(scalbn(rowbuf[c], sc)) : 0.0f;
+                crow[q] = c < n ? __double2float_rn(scalbn(rowbuf[c], sc)) : 0.0f; // pads 0
             }
         }
         if (p.choice_perm64) {
