@@ -175,6 +175,15 @@ aco_status aco_gpu_get_info(aco_gpu_ctx* ctx, int32_t* m, int32_t* ant_begin, in
 /* The cudaStream_t (as void*) every kernel of this context runs on, so a
  * caller can time it with CUDA events on the launching stream. */
 void* aco_gpu_stream(aco_gpu_ctx* ctx);
+/* Exchange buffers of a sharded context (world > 1), device pointers:
+ *   succ/pred [world][n][S] int32 (gather deposits), inv [world][S] fp64
+ *   (1/C_k), delta n x P64 fp64 (accumulate).  With world > 1 and an all-zero
+ *   nccl_id the context runs in EXTERNAL-EXCHANGE mode: aco_gpu_construct
+ *   fills this rank's shard (and its local delta), the caller performs the
+ *   all-gather / all-reduce itself, then calls aco_gpu_update.  (Used to test
+ *   the sharded device path on one GPU; statistics are per shard.) */
+aco_status aco_gpu_exchange_buffers(aco_gpu_ctx* ctx, void** succ, void** pred, void** inv,
+                                    void** delta, int32_t* shard_stride, int32_t* P64);
 /* Number of kernel launches issued by this context since creation. */
 int64_t aco_gpu_launch_count(const aco_gpu_ctx* ctx);
 

@@ -58,7 +58,7 @@ EXPORTS = [
     "aco_gpu_last_error", "aco_gpu_set_pheromone", "aco_gpu_compute_choice_info",
     "aco_gpu_construct", "aco_gpu_update", "aco_gpu_iterate", "aco_gpu_get_pheromone",
     "aco_gpu_get_choice", "aco_gpu_get_choice32", "aco_gpu_get_tours", "aco_gpu_get_best",
-    "aco_gpu_get_info", "aco_gpu_stream", "aco_gpu_launch_count", "aco_gpu_nccl_unique_id",
+    "aco_gpu_get_info", "aco_gpu_stream", "aco_gpu_exchange_buffers", "aco_gpu_launch_count", "aco_gpu_nccl_unique_id",
     "aco_gpu_philox_uniform",
 ]
 
@@ -102,6 +102,8 @@ def _load() -> C.CDLL:
                                    C.POINTER(C.c_double), C.POINTER(_i32), C.POINTER(_i32)]
     L.aco_gpu_stream.argtypes = [_p]
     L.aco_gpu_stream.restype = C.c_void_p
+    L.aco_gpu_exchange_buffers.argtypes = [_p, C.POINTER(_p), C.POINTER(_p), C.POINTER(_p),
+                                           C.POINTER(_p), C.POINTER(_i32), C.POINTER(_i32)]
     L.aco_gpu_launch_count.argtypes = [_p]
     L.aco_gpu_launch_count.restype = C.c_int64
     L.aco_gpu_nccl_unique_id.argtypes = [_p]

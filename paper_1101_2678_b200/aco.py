@@ -404,6 +404,15 @@ class Engine:
         """cudaStream_t of this engine (for CUDA-event timing on the launching stream)."""
         return lib.aco_gpu_stream(self._h)
 
+    def exchange_buffers(self):
+        """Device pointers of the shard exchange buffers (aco_gpu_exchange_buffers)."""
+        ps = [C.c_void_p() for _ in range(4)]
+        S, P64 = C.c_int32(), C.c_int32()
+        _check(lib.aco_gpu_exchange_buffers(self._h, *[C.byref(x) for x in ps], C.byref(S),
+                                            C.byref(P64)), self._h)
+        return {"succ": ps[0].value, "pred": ps[1].value, "inv": ps[2].value,
+                "delta": ps[3].value, "S": S.value, "P64": P64.value}
+
     def launch_count(self) -> int:
         return lib.aco_gpu_launch_count(self._h)
 

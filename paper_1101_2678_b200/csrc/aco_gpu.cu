@@ -121,6 +121,7 @@ struct aco_gpu_ctx {
     unsigned long long* d_timing = nullptr; // ACO_TIMING phase cycles
     long long* h_stats = nullptr;       // pinned: 4 stats + 2 fallback counters
     ncclComm_t comm = nullptr;
+    bool external = false; // world > 1 without an NCCL id: the caller exchanges
 };
 
 namespace {
@@ -347,13 +348,19 @@ void do_construct(aco_gpu_ctx* c) {
         c->d_len, c->mloc, c->d_tours, c->n, c->d_stats, c->d_stats + 3, c->d_best,
         c->world == 1 ? 1 : 0);
     check_launch(c, "k_iter_stats");
+    if (c->world > 1 && !gather_mode(c)) { // local delta for the all-reduce
+        k_deposit_atomic<<<c->num_sms * 8, 256, 0, c->stream>>>(
+            c->d_tours, c->d_inv + static_cast<size_t>(c->rank) * c->S, c->n, c->P64, c->mloc,
+            c->d_delta);
+        check_launch(c, "k_deposit_atomic");
+    }
     CK(cudaEventRecord(c->ev[2], c->stream));
 }
 
 // exchange + evaporate + deposit + choice (no host sync)
 void do_update(aco_gpu_ctx* c) {
     const double keep = 1.0 - c->cfg.rho;
-    if (c->world > 1) {
+    if (c->world > 1 && !c->external) {
         auto& api = nccl();
         if (gather_mode(c)) {
             const size_t blk = static_cast<size_t>(c->n) * c->S;
@@ -364,9 +371,6 @@ void do_update(aco_gpu_ctx* c) {
                              ncclFloat64, c->comm, c->stream));
             NK(api.GroupEnd());
         } else {
-            k_deposit_atomic<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_tours, c->d_inv + static_cast<size_t>(c->rank) * c->S,
-                                                                    c->n, c->P64, c->mloc, c->d_delta);
-            check_launch(c, "k_deposit_atomic");
             NK(api.AllReduce(c->d_delta, c->d_delta, static_cast<size_t>(c->n) * c->P64,
                              ncclFloat64, ncclSum, c->comm, c->stream));
         }
@@ -400,7 +404,7 @@ float ev_ms(aco_gpu_ctx* c, int a, int b) {
 // Reads stats; for world > 1 reduces them over NCCL (best, then owner, sum)
 // and broadcasts the improving tour.
 void finish_stats(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
-    if (c->world > 1) {
+    if (c->world > 1 && !c->external) {
         auto& api = nccl();
         long long* s = c->d_stats;
         // s[0] best len (local), s[1] best local ant, s[2] sum.
@@ -432,7 +436,7 @@ void finish_stats(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
             }
             NK(api.Broadcast(c->d_best, c->d_best, c->n + 1, ncclInt32, owner, c->comm, c->stream));
         }
-    } else {
+    } else { // one shard (external mode: this shard's own statistics)
         rec->best_length = c->h_stats[0];
         rec->mean_length = static_cast<double>(c->h_stats[2]) / static_cast<double>(c->mloc);
         c->best_so_far = std::min<int64_t>(c->best_so_far, c->h_stats[0]);
@@ -660,6 +664,11 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         CK(cudaMallocHost(&c->h_stats, 8 * sizeof(long long)));
 
         if (c->world > 1) {
+            bool zero = true;
+            for (int i = 0; i < 128; ++i) zero = zero && prm->nccl_id[i] == 0;
+            c->external = zero;
+        }
+        if (c->world > 1 && !c->external) {
             auto& api = nccl();
             if (!api.CommInitRank) throw Fail{ACO_E_NCCL, "libnccl.so.2 not found"};
             ncclUniqueId id;
@@ -718,6 +727,18 @@ const char* aco_gpu_last_error(const aco_gpu_ctx* c) { return c ? c->err.c_str()
 int64_t aco_gpu_launch_count(const aco_gpu_ctx* c) { return c ? c->launches : 0; }
 
 void* aco_gpu_stream(aco_gpu_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+aco_status aco_gpu_exchange_buffers(aco_gpu_ctx* c, void** succ, void** pred, void** inv,
+                                    void** delta, int32_t* shard_stride, int32_t* P64) {
+    if (!c) return ACO_E_CONFIG_ERROR;
+    if (succ) *succ = c->d_succ;
+    if (pred) *pred = c->d_pred;
+    if (inv) *inv = c->d_inv;
+    if (delta) *delta = c->d_delta;
+    if (shard_stride) *shard_stride = c->S;
+    if (P64) *P64 = c->P64;
+    return ACO_OK;
+}
 
 aco_status aco_gpu_set_pheromone(aco_gpu_ctx* c, const double* tau) {
     return guard_ctx(c, [&] {
@@ -778,7 +799,7 @@ aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* to
         aco_gpu_iter_record* r = rec ? rec : &tmp;
         fill_common(c, r);
         do_construct(c);
-        if (c->world > 1) {
+        if (c->world > 1 && !c->external) {
             // stats must be reduced before the best tour can be broadcast
             CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
             finish_stats(c, r);
@@ -790,11 +811,11 @@ aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* to
         if (lengths_out)
             CK(cudaMemcpyAsync(lengths_out, c->d_len, sizeof(int64_t) * c->mloc,
                                cudaMemcpyDeviceToHost, c->stream));
-        if (c->world == 1)
+        if (c->world == 1 || c->external)
             CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(c->h_stats + 6, c->d_fb, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
-        if (c->world == 1) finish_stats(c, r);
+        if (c->world == 1 || c->external) finish_stats(c, r);
         r->construct_ms = ev_ms(c, 0, 2);
         r->construct_kernel_ms = ev_ms(c, 0, 1);
         r->update_ms = ev_ms(c, 2, 5);

@@ -1,0 +1,91 @@
+"""The ant-sharded device path on ONE GPU: G contexts in external-exchange
+mode (world = G, zero NCCL id) each construct their ant shard; the test
+performs the all-gather / all-reduce the engine would run over NCCL, then
+every context updates.  Tours must equal the single-context colony
+bit-for-bit, the gather-path tau must be bit-identical on every shard, and
+the atomic-path tau must agree within 1e-5 (the order of the Δτ reduction
+differs)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+class DevArray:
+    """__cuda_array_interface__ view of a raw device pointer (for torch.as_tensor)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3}
+
+
+def _engines(aco, n, m, deposit, G):
+    spec = aco.synthetic_instance(n)
+    prob = aco.build_problem(spec)
+
+    def cfg(world=1, rank=0):
+        return aco.RunConfig(params=aco.Parameters(m=m, seed=3),
+                             selection=aco.SelectionStrategy(aco.Selection.roulette_full),
+                             deposit=aco.DepositStrategy(aco.Deposit(deposit)),
+                             world=world, rank=rank)
+
+    single = aco.Engine(prob, cfg())
+    shards = [aco.Engine(prob, cfg(G, r)) for r in range(G)]
+    return prob, single, shards
+
+
+@pytest.mark.parametrize("deposit", [1, 0])
+@pytest.mark.parametrize("G,m", [(2, 300), (3, 301)])
+def test_virtual_shards_match_single_context(deposit, G, m):
+    import torch
+
+    from paper_1101_2678_b200 import aco
+
+    n = 300
+    prob, single, shards = _engines(aco, n, m, deposit, G)
+    bufs = [e.exchange_buffers() for e in shards]
+    S = bufs[0]["S"]
+    P64 = bufs[0]["P64"]
+    for it in range(3):
+        single.run_iteration()
+        t_ref, l_ref = single.ants()
+        for e in shards:
+            e.construct()
+        torch.cuda.synchronize()
+        got = np.concatenate([e.ants()[0] for e in shards])
+        assert np.array_equal(got, t_ref), f"tours differ at iteration {it}"
+        if deposit != 0:  # all-gather the shard blocks (succ, pred, 1/C_k)
+            blk = n * S
+            for name, typ, width in (("succ", "<i4", blk), ("pred", "<i4", blk), ("inv", "<f8", S)):
+                views = [torch.as_tensor(DevArray(b[name], (G * width,), typ), device="cuda")
+                         for b in bufs]
+                for r in range(G):
+                    src = views[r][r * width:(r + 1) * width]
+                    for q in range(G):
+                        if q != r:
+                            views[q][r * width:(r + 1) * width].copy_(src)
+        else:  # all-reduce the local deltas
+            views = [torch.as_tensor(DevArray(b["delta"], (n * P64,), "<f8"), device="cuda")
+                     for b in bufs]
+            total = torch.zeros_like(views[0])
+            for v in views:
+                total += v
+            for v in views:
+                v.copy_(total)
+        torch.cuda.synchronize()
+        for e in shards:
+            e.update()
+        tau_ref = single.pheromone()
+        for e in shards:
+            tau = e.pheromone()
+            if deposit != 0:
+                assert np.array_equal(tau, tau_ref), "gather tau must be bit-identical"
+            else:
+                assert np.max(np.abs(tau - tau_ref) / np.abs(tau_ref)) <= 1e-5
+            if deposit != 0:
+                assert np.array_equal(e.choice(), single.choice())
+        if deposit == 0:  # keep the colonies on the same trajectory
+            for e in shards:
+                e.set_pheromone(tau_ref)
+    for e in shards + [single]:
+        e.close()
