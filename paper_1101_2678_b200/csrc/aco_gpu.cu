@@ -12,6 +12,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -303,6 +304,9 @@ void launch_construct(aco_gpu_ctx* c) {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem));
         const int grid = std::max(1, std::min(c->mloc, per_sm * c->num_sms));
         c->construct_grid = grid;
+        if (std::getenv("ACO_DEBUG"))
+            std::fprintf(stderr, "construct: NV=%d MAXR=%d smem=%zu per_sm=%d grid=%d\n", c->NV,
+                         c->MAXR, smem, per_sm, grid);
         fn<<<grid, 32, smem, c->stream>>>(p);
         check_launch(c, "k_construct_roulette");
     } else if (c->cfg.selection == ACO_SEL_NN) {
