@@ -212,6 +212,12 @@ class Reference:
                                                      C.c_double, C.POINTER(C.c_int),
                                                      C.POINTER(C.c_double)]
 
+    def format_double(self, v: float) -> str:
+        buf = C.create_string_buffer(64)
+        self.lib.ref_format_double.argtypes = [C.c_double, C.c_char_p]
+        self.lib.ref_format_double(v, buf)
+        return buf.value.decode()
+
     def _check(self, rc):
         if rc:
             raise RuntimeError(f"reference rc={rc}: {self.lib.ref_last_error().decode()}")

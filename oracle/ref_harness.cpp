@@ -14,11 +14,15 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "aco/engine.hpp"
+#ifdef ACO_REF_WITH_JSON
+#include "aco/report.hpp" // needs nlohmann/json.hpp (vendored in the image's cudnn_frontend)
+#endif
 
 namespace {
 
@@ -337,5 +341,13 @@ int ref_verify_deposit_equivalence(int n, const double* xs, const double* ys, in
         *worst = w;
     });
 }
+
+#ifdef ACO_REF_WITH_JSON
+void ref_format_double(double v, char* out) {
+    const std::string s = aco::format_double(v);
+    std::memcpy(out, s.c_str(), s.size() + 1);
+}
+
+#endif
 
 } // extern "C"

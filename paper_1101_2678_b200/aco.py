@@ -458,6 +458,62 @@ def run(config: RunConfig) -> RunReport:  # engine.hpp:198-204
     return rep
 
 
+@dataclass
+class MatrixDiff:  # pheromone.hpp:400-404
+    max_abs_diff: float = 0.0
+    i: int = 0
+    j: int = 0
+
+
+def max_cell_difference(a: np.ndarray, b: np.ndarray) -> MatrixDiff:  # pheromone.hpp:406
+    d = np.abs(a - b)
+    k = int(np.argmax(d))
+    if d.flat[k] <= 0.0:
+        return MatrixDiff()
+    return MatrixDiff(float(d.flat[k]), k // a.shape[1], k % a.shape[1])
+
+
+@dataclass
+class VerifyReport:  # engine.hpp:212-228
+    strategies: list = field(default_factory=list)  # (variant, measured ledger, predicted, ok)
+    pairs: list = field(default_factory=list)       # (a, b, MatrixDiff, pass)
+    all_pass: bool = False
+
+
+def verify_deposit_equivalence(problem: ProblemInstance, config: RunConfig,
+                               tolerance: float = 1e-9) -> VerifyReport:
+    """engine.hpp:227-295 on the GPU: one iteration-0 construction (identical
+    in every engine: the draws are keyed by (seed, iteration, ant, step)),
+    then each deposit variant from the same tau0; pairwise max cell
+    difference <= tolerance and ledger == predicted_access_cost."""
+    variants = [Deposit.accumulate, Deposit.scatter_gather, Deposit.scatter_gather_tiled,
+                Deposit.symmetric_reduction]
+    results, rep = [], VerifyReport()
+    tours0 = None
+    for v in variants:
+        cfg = RunConfig(params=config.params, selection=config.selection,
+                        deposit=DepositStrategy(v, config.params.tile_size),
+                        random_start=False, device=config.device, stream=config.stream)
+        with Engine(problem, cfg) as eng:
+            rec = eng.run_iteration()
+            t, _ = eng.ants()
+            if tours0 is None:
+                tours0 = t
+            elif not np.array_equal(t, tours0):
+                raise Error(Errc.inconsistent_length, "engines built different tours")
+            results.append(eng.pheromone())
+            pred = predicted_access_cost(cfg.deposit, problem.n, eng.m, config.params.tile_size)
+            rep.strategies.append((v, rec.deposit_ledger, pred, rec.deposit_ledger == pred))
+    rep.all_pass = all(s[3] for s in rep.strategies)
+    for a in range(len(variants)):
+        for b in range(a + 1, len(variants)):
+            d = max_cell_difference(results[a], results[b])
+            ok = d.max_abs_diff <= tolerance
+            rep.pairs.append((variants[a], variants[b], d, ok))
+            rep.all_pass = rep.all_pass and ok
+    return rep
+
+
 def philox_uniform_device(seed: int, iteration: int, ant: int, steps, draws, device: int = 0):
     """Device Philox draws (rng.hpp:74-80) for unit parity tests."""
     st = np.ascontiguousarray(steps, np.uint32)

@@ -95,6 +95,16 @@ def main():
                             "ants": ants, "roulette_tours_fnv": fnv1a64(t),
                             "roulette_lengths": l.tolist(), "nn_tours_fnv": fnv1a64(tn),
                             "nn_lengths": ln.tolist()}
+    # the reference's own RunReport JSON / bench CSV (report.hpp) for synth198
+    import subprocess
+    here = os.path.dirname(os.path.abspath(__file__))
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "_ref/ref_report"], check=True)
+    xs, ys = synth_coords(198)
+    coords = f"{len(xs)}\n" + "".join(f"{x:.1f} {y:.1f}\n" for x, y in zip(xs, ys))
+    for dep in (1, 3):
+        subprocess.run([os.path.join(ROOT, "oracle", "_ref", "ref_report"),
+                        os.path.join(here, f"report_synth198_dep{dep}"), str(dep), "6"],
+                       input=coords.encode(), check=True)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
