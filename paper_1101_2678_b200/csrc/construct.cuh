@@ -64,28 +64,29 @@ template <> struct VecOf<double> {
     static constexpr int V = 2;
 };
 
-// Physical layout of a streamed row: LP = 33 vector slots per line (32 lanes
-// + 1 pad slot) so that a warp reading one lane's chunk (the crossing walk)
-// spreads over 8 bank groups instead of one.  Round r holds cities
-// [r*32C, (r+1)*32C) in LP*C elements.
-constexpr int kLP = 33;
+// Physical layout of a streamed row.  LA lanes share a row (32: one ant per
+// warp; 16: two ants per warp), each owning C contiguous cities; a line of
+// vectors has LA + 1 slots (one pad slot) so that reading one lane's chunk
+// across a warp spreads over several bank groups.  Round r holds cities
+// [r*LA*C, (r+1)*LA*C) in (LA+1)*C elements.
+constexpr int kLP = 33; // (LA + 1) for LA = 32
 
-__host__ __device__ __forceinline__ int stream_pos(int c, int C, int V) {
-    const int R32 = 32 * C;
-    const int r = c / R32, rem = c - r * R32;
+__host__ __device__ __forceinline__ int stream_pos(int c, int C, int V, int LA = 32) {
+    const int RC = LA * C, LP = LA + 1;
+    const int r = c / RC, rem = c - r * RC;
     const int l = rem / C, e = rem - l * C;
     const int t = e / V, q = e - t * V;
-    return r * (kLP * C) + (t * kLP + l) * V + q;
+    return r * (LP * C) + (t * LP + l) * V + q;
 }
 
 // Inverse of stream_pos; returns INT_MAX for pad slots.
-__host__ __device__ __forceinline__ int stream_city(int p, int C, int V) {
-    const int RS = kLP * C;
+__host__ __device__ __forceinline__ int stream_city(int p, int C, int V, int LA = 32) {
+    const int LP = LA + 1, RS = LP * C;
     const int r = p / RS, rem = p - r * RS;
-    const int t = rem / (kLP * V), rem2 = rem - t * kLP * V;
+    const int t = rem / (LP * V), rem2 = rem - t * LP * V;
     const int l = rem2 / V, q = rem2 - l * V;
-    if (l >= 32) return 0x7fffffff;
-    return r * 32 * C + l * C + t * V + q;
+    if (l >= LA) return 0x7fffffff;
+    return r * LA * C + l * C + t * V + q;
 }
 
 struct ConstructParams {
@@ -104,6 +105,7 @@ struct ConstructParams {
     uint32_t iteration;
     uint64_t seed;
     unsigned long long* timing; // ACO_TIMING: [8] phase cycle totals
+    int half_smem;              // two-ants-per-warp kernel: bytes of one half's shared area
 };
 
 __device__ __forceinline__ bool tabu_test(const uint32_t* tabu, int j) {

@@ -162,7 +162,7 @@ struct RowParams {
     const int32_t* nn_lists; // n x nn (nn selection) or null
     double* choice_nn;       // n x nn: choice64[i][nn_lists[i][q]] (nn selection)
     int nn;
-    int n, P64, PW, C, V;
+    int n, P64, PW, C, V, LA;
     int shards, S, m;        // ants: shard g holds global ants [g*S, min(m,(g+1)*S))
     double alpha, keep;
 };
@@ -254,14 +254,14 @@ __global__ void __launch_bounds__(256) k_rows(RowParams p) {
             if (tid == 0) p.scale_exp[i] = sc;
             float* crow = p.choice32 + static_cast<size_t>(i) * p.PW;
             for (int q = tid; q < p.PW; q += blockDim.x) {
-                const int c = stream_city(q, p.C, 4);
+                const int c = stream_city(q, p.C, 4, p.LA);
                 crow[q] = c < n ? __double2float_rn(scalbn(rowbuf[c], sc)) : 0.0f; // pads 0
             }
         }
         if (p.choice_perm64) {
             double* crow = p.choice_perm64 + static_cast<size_t>(i) * p.PW;
             for (int q = tid; q < p.PW; q += blockDim.x) {
-                const int c = stream_city(q, p.C, 2);
+                const int c = stream_city(q, p.C, 2, p.LA);
                 crow[q] = c < n ? rowbuf[c] : 0.0;
             }
         }
