@@ -192,6 +192,7 @@ ConstructFn pick_roulette(int NV, int MAXR) {
         case 8: return k_construct_roulette<WT, 8, 1>;
         case 12: return k_construct_roulette<WT, 12, 1>;
         case 16: return k_construct_roulette<WT, 16, 1>;
+        case 19: return k_construct_roulette<WT, 19, 1>;
         default: return k_construct_roulette<WT, 20, 1>;
         }
     }
@@ -226,7 +227,7 @@ void choose_stream_layout(aco_gpu_ctx* c) {
         return;
     }
     c->LA = 32;
-    static const int nvs[] = {2, 4, 8, 12, 16, 20};
+    static const int nvs[] = {2, 4, 8, 12, 16, 19, 20};
     c->NV = 0;
     for (int nv : nvs)
         if (32 * nv * c->V >= c->n) {

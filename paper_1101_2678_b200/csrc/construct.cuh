@@ -43,6 +43,9 @@
 #ifndef ACO_LDG
 #define ACO_LDG 2 // 1: ld.global.nc.L1::no_allocate; 2: ld.global.nc (L1-allocating)
 #endif
+#ifndef ACO_ROW_SRC
+#define ACO_ROW_SRC 0 // fp32 single-round roulette: 0 = TMA row staging, 1 = L1-allocating LDG
+#endif
 #ifndef ACO_TIMING
 #define ACO_TIMING 0 // per-phase clock64() accounting into ConstructParams::timing
 #endif
@@ -266,6 +269,25 @@ __device__ __forceinline__ float tree_sum_packed(float (&x)[N]) {
     return y[0].x + y[0].y;
 }
 
+// Inclusive warp scan step without a lane-index compare: shfl.sync.up's
+// predicate output says whether the source lane existed.
+__device__ __forceinline__ float scan_up_add(float v, int off) {
+    float y;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "shfl.sync.up.b32 %0|p, %1, %2, 0, -1;\n\t"
+        "@p add.rn.f32 %0, %0, %1;\n\t"
+        "@!p mov.b32 %0, %1;\n}"
+        : "=f"(y)
+        : "f"(v), "r"(off));
+    return y;
+}
+__device__ __forceinline__ float warp_inclusive_scan(float v) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) v = scan_up_add(v, off);
+    return v;
+}
+
 template <int C>
 __host__ __device__ constexpr int ceil_log2() {
     int d = 0;
@@ -438,6 +460,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
     constexpr int GE = GV * V;                         // cities per group
     constexpr int D1 = ceil_log2<GE>() + ceil_log2<NG>();
     constexpr bool F32 = sizeof(WT) == 4;
+    constexpr bool kLDG = (ACO_ROW_SRC == 1) && F32 && MAXR == 1; // rows via L1, not smem
     static_assert(GE <= 32 && 32 % GE == 0, "a group's bits live in one window word");
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -489,10 +512,11 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
 #endif
 
         for (int step = 1; step < n; ++step) {
-            if (!prefetched && lane == 0) {
+            const WT* __restrict__ grow = wbase + static_cast<size_t>(cur) * p.PW;
+            if (!kLDG && !prefetched && lane == 0) {
                 fence_proxy_async_smem(); // generic reads of buf happen-before the refill
                 mbar_expect_tx(bar, row_bytes);
-                tma_row(buf, wbase + static_cast<size_t>(cur) * p.PW, row_bytes, bar);
+                tma_row(buf, grow, row_bytes, bar);
             }
             // Draw 0 of steps step..step+31: lane i holds step + i (rng.hpp:74-80).
             if (((step - 1) & 31) == 0)
@@ -500,9 +524,12 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                                         static_cast<uint32_t>(step + lane), 0);
             const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
             __syncwarp();
-            mbar_wait(bar, phase);
-            phase ^= 1u;
+            if (!kLDG) {
+                mbar_wait(bar, phase);
+                phase ^= 1u;
+            }
             prefetched = false;
+            const WT* rowsrc = kLDG ? grow : buf; // where this step reads the row
             TICK(6);
 
             AT incl[MAXR];
@@ -521,7 +548,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
 #pragma unroll
                     for (int i = 0; i < NWIN; ++i)
                         win[i] = __funnelshift_r(tabu[w0 + i], tabu[w0 + i + 1], sh);
-                    const VT* rv = reinterpret_cast<const VT*>(buf + r * kLP * C) + lane;
+                    const VT* rv = reinterpret_cast<const VT*>(rowsrc + r * kLP * C) + lane;
                     WT gs[NG];
 #pragma unroll
                     for (int g = 0; g < NG; ++g) {
@@ -531,7 +558,8 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                             const int tv = g * GV + tt;
                             VT v;
                             if (tv < NV) {
-                                v = rv[tv * kLP];
+                                if constexpr (kLDG) v = __ldg(rv + tv * kLP);
+                                else v = rv[tv * kLP];
                             } else {
                                 if constexpr (F32) v = make_float4(0.f, 0.f, 0.f, 0.f);
                                 else v = make_double2(0.0, 0.0);
@@ -560,10 +588,14 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                     }
                     AT d = static_cast<AT>(tree_sum<WT, NG>(gs));
                     TICK(0);
+                    if constexpr (F32) {
+                        d = warp_inclusive_scan(d);
+                    } else {
 #pragma unroll
-                    for (int off = 1; off < 32; off <<= 1) {
-                        const AT y = __shfl_up_sync(kFull, d, off);
-                        if (lane >= off) d += y;
+                        for (int off = 1; off < 32; off <<= 1) {
+                            const AT y = __shfl_up_sync(kFull, d, off);
+                            if (lane >= off) d += y;
+                        }
                     }
                     incl[r] = d;
                     rtot[r] = __shfl_sync(kFull, d, 31);
@@ -609,62 +641,70 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                     const AT exclL = base + (L == 0 ? AT(0) : myprev);
                     constexpr int NQT = C / 4; // quads per chunk
                     const int cbaseL = rs * 32 * C + L * C;
-                    AT xv[4] = {AT(0), AT(0), AT(0), AT(0)};
-                    if (lane < NQT) {
-                        const int e0 = 4 * lane;
-                        if constexpr (F32) {
-                            const float4 v = *reinterpret_cast<const float4*>(
-                                buf + rs * kLP * C + (lane * kLP + L) * 4);
-                            xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
-                        } else {
-                            const double2 v0 = *reinterpret_cast<const double2*>(
-                                buf + rs * kLP * C + ((2 * lane) * kLP + L) * 2);
-                            const double2 v1 = *reinterpret_cast<const double2*>(
-                                buf + rs * kLP * C + ((2 * lane + 1) * kLP + L) * 2);
-                            xv[0] = v0.x; xv[1] = v0.y; xv[2] = v1.x; xv[3] = v1.y;
-                        }
-                        const int c0 = cbaseL + e0;
-                        const uint32_t bits4 =
+                    // all lanes load (lanes >= NQT re-read quad 0 and drop it)
+                    const int ql = lane < NQT ? lane : 0;
+                    AT xv[4];
+                    if constexpr (F32) {
+                        const float4* qp = reinterpret_cast<const float4*>(
+                            rowsrc + rs * kLP * C + (ql * kLP + L) * 4);
+                        float4 v;
+                        if constexpr (kLDG) v = __ldg(qp);
+                        else v = *qp;
+                        xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
+                    } else {
+                        const double2 v0 = *reinterpret_cast<const double2*>(
+                            buf + rs * kLP * C + ((2 * ql) * kLP + L) * 2);
+                        const double2 v1 = *reinterpret_cast<const double2*>(
+                            buf + rs * kLP * C + ((2 * ql + 1) * kLP + L) * 2);
+                        xv[0] = v0.x; xv[1] = v0.y; xv[2] = v1.x; xv[3] = v1.y;
+                    }
+                    {
+                        const int c0 = cbaseL + 4 * ql;
+                        uint32_t bits4 =
                             __funnelshift_r(tabu[c0 >> 5], tabu[(c0 >> 5) + 1], c0 & 31);
+                        if (lane >= NQT) bits4 = 0xFu;
 #pragma unroll
                         for (int q = 0; q < 4; ++q)
                             if ((bits4 >> q) & 1u) xv[q] = AT(0);
                     }
                     const AT qs = (xv[0] + xv[1]) + (xv[2] + xv[3]);
                     AT qi = qs;
+                    if constexpr (F32) {
+                        qi = warp_inclusive_scan(qi);
+                    } else {
 #pragma unroll
-                    for (int off = 1; off < 32; off <<= 1) {
-                        const AT y = __shfl_up_sync(kFull, qi, off);
-                        if (lane >= off) qi += y;
+                        for (int off = 1; off < 32; off <<= 1) {
+                            const AT y = __shfl_up_sync(kFull, qi, off);
+                            if (lane >= off) qi += y;
+                        }
                     }
                     const AT qe = __shfl_up_sync(kFull, qi, 1);
                     const unsigned qb = __ballot_sync(kFull, lane < NQT && exclL + qi > t);
                     Q = __ffs(qb) - 1;
-                    if (lane == Q) {
-                        AT ea = exclL + (lane == 0 ? AT(0) : qe);
-                        AT Pj32 = AT(0), Pp32 = AT(0);
-                        int E = -1;
+                    // every lane walks its own quad; only lane Q's result is kept
+                    AT ea = exclL + (lane == 0 ? AT(0) : qe);
+                    AT Pj32 = AT(0), Pp32 = AT(0);
+                    int E = -1;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const AT na = ea + xv[q];
-                            const bool hit = (E < 0) && (xv[q] > AT(0)) && (na > t);
-                            Pj32 = hit ? na : Pj32;
-                            Pp32 = hit ? ea : Pp32;
-                            E = hit ? q : E;
-                            ea = na;
-                        }
-                        if (E >= 0) {
-                            J = cbaseL + 4 * lane + E;
-                            const double Pj = static_cast<double>(Pj32);
-                            const double Pprev = static_cast<double>(Pp32);
-                            cert = (Pj * lo_f > A) && (Pprev + e_rel * Pj < B) && J < n;
-                        }
+                    for (int q = 0; q < 4; ++q) {
+                        const AT na = ea + xv[q];
+                        const bool hit = (E < 0) && (xv[q] > AT(0)) && (na > t);
+                        Pj32 = hit ? na : Pj32;
+                        Pp32 = hit ? ea : Pp32;
+                        E = hit ? q : E;
+                        ea = na;
                     }
+                    const double Pj = static_cast<double>(Pj32);
+                    const double Pprev = static_cast<double>(Pp32);
+                    const int Jc = cbaseL + 4 * lane + E;
+                    const bool mine = (lane == Q) && (E >= 0);
+                    J = mine ? Jc : -1;
+                    cert = mine && (Pj * lo_f > A) && (Pprev + e_rel * Pj < B) && Jc < n;
                 }
                 TICK(2);
                 // speculative refill, issued by the certifying lane itself: every
                 // read of buf in this step has returned (its value fed the ballots)
-                if (cert && step + 1 < n) {
+                if (!kLDG && cert && step + 1 < n) {
                     mbar_expect_tx(bar, row_bytes);
                     tma_row(buf, wbase + static_cast<size_t>(J) * p.PW, row_bytes, bar);
                 }
@@ -672,10 +712,26 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                 ok = cb != 0u;
                 if (ok) {
                     next = __shfl_sync(kFull, J, __ffs(cb) - 1);
-                    prefetched = step + 1 < n;
+                    prefetched = !kLDG && step + 1 < n;
+                    if (kLDG && step + 1 < n) { // speculative L1 prefetch of the next row
+                        const char* nr = reinterpret_cast<const char*>(wbase + static_cast<size_t>(next) * p.PW);
+                        for (int ln = lane; ln * 128 < static_cast<int>(row_bytes); ln += 32)
+                            asm volatile("prefetch.global.L1 [%0];" ::"l"(nr + ln * 128));
+                    }
                 }
             }
             TICK(3);
+            if (kLDG && !ok) { // tier 2 reads the row from smem: stage it now
+                __syncwarp();
+                if (lane == 0) {
+                    fence_proxy_async_smem();
+                    mbar_expect_tx(bar, row_bytes);
+                    tma_row(buf, grow, row_bytes, bar);
+                }
+                __syncwarp();
+                mbar_wait(bar, phase);
+                phase ^= 1u;
+            }
             if (!ok) { // middle tier: fp64 sums over the fp32 row still in smem
                 const int j2 = certify_fp64<WT, NV, MAXR>(buf, tabu, n, p.R, u, lane);
                 if (j2 >= 0) {
