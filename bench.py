@@ -280,6 +280,7 @@ def run_ours(args):
         e2e.append((time.perf_counter() - t0) * 1e3)
     e2e_ms = max_over_ranks(statistics.mean(e2e))
     d2h = tours_h.nbytes + lens_h.nbytes
+    kernel_desc = eng.describe()
     eng.close()
 
     # ---- deterministic scatter-to-gather deposit, same workload
@@ -338,7 +339,7 @@ def run_ours(args):
                                        "update_ms": round(upd_g, 4),
                                        "tau": "bit-exact vs reference"},
                     "accumulate": {"tau": "atomic, <=1e-5 relative vs reference"}},
-        "roofline": {"bound": "l2", "kernel": "k_construct_roulette<float,20,1>",
+        "roofline": {"bound": "l2", "kernel": kernel_desc,
                      "achieved": round(achieved, 1), "peak": l2_peak, "unit": "GB/s",
                      "frac": round(achieved / l2_peak, 4) if l2_peak else None,
                      "traffic": traffic,

@@ -184,6 +184,11 @@ void* aco_gpu_stream(aco_gpu_ctx* ctx);
  *   the sharded device path on one GPU; statistics are per shard.) */
 aco_status aco_gpu_exchange_buffers(aco_gpu_ctx* ctx, void** succ, void** pred, void** inv,
                                     void** delta, int32_t* shard_stride, int32_t* P64);
+/* Human-readable name + launch shape of the last construction kernel
+ * (e.g. "k_construct_roulette<float,19,1> grid=2392 per_sm=17 ..."); copies at
+ * most len-1 bytes + NUL into buf, returns the full length.  Empty before the
+ * first construction.  (No reference counterpart: diagnostics for bench.py.) */
+int32_t aco_gpu_describe(const aco_gpu_ctx* ctx, char* buf, int32_t len);
 /* Number of kernel launches issued by this context since creation. */
 int64_t aco_gpu_launch_count(const aco_gpu_ctx* ctx);
 

@@ -58,7 +58,7 @@ EXPORTS = [
     "aco_gpu_last_error", "aco_gpu_set_pheromone", "aco_gpu_compute_choice_info",
     "aco_gpu_construct", "aco_gpu_update", "aco_gpu_iterate", "aco_gpu_get_pheromone",
     "aco_gpu_get_choice", "aco_gpu_get_choice32", "aco_gpu_get_tours", "aco_gpu_get_best",
-    "aco_gpu_get_info", "aco_gpu_stream", "aco_gpu_exchange_buffers", "aco_gpu_launch_count", "aco_gpu_nccl_unique_id",
+    "aco_gpu_get_info", "aco_gpu_stream", "aco_gpu_exchange_buffers", "aco_gpu_launch_count", "aco_gpu_describe", "aco_gpu_nccl_unique_id",
     "aco_gpu_philox_uniform",
 ]
 
@@ -106,6 +106,8 @@ def _load() -> C.CDLL:
                                            C.POINTER(_p), C.POINTER(_i32), C.POINTER(_i32)]
     L.aco_gpu_launch_count.argtypes = [_p]
     L.aco_gpu_launch_count.restype = C.c_int64
+    L.aco_gpu_describe.argtypes = [_p, C.c_char_p, C.c_int32]
+    L.aco_gpu_describe.restype = C.c_int32
     L.aco_gpu_nccl_unique_id.argtypes = [_p]
     L.aco_gpu_philox_uniform.argtypes = [_i32, C.c_uint64, C.c_uint32, C.c_uint32, _i32, _p, _p,
                                          _p]

@@ -416,6 +416,13 @@ class Engine:
     def launch_count(self) -> int:
         return lib.aco_gpu_launch_count(self._h)
 
+    def describe(self) -> str:
+        """Kernel name and launch shape of the last construction (diagnostics)."""
+        import ctypes
+        buf = ctypes.create_string_buffer(256)
+        lib.aco_gpu_describe(self._h, buf, 256)
+        return buf.value.decode()
+
     # -- the iteration (engine.hpp:88-157)
     @staticmethod
     def _record(r: _lib.aco_gpu_iter_record) -> IterationRecord:

@@ -95,6 +95,7 @@ struct aco_gpu_ctx {
     int64_t max_d = 0;
     int device = 0, num_sms = 0;
     int construct_grid = 0;
+    std::string construct_desc;  // kernel + launch shape of the last construction
     int iteration = 0;
     int64_t best_so_far = std::numeric_limits<int64_t>::max();
     int64_t launches = 0;
@@ -339,9 +340,11 @@ void launch_construct(aco_gpu_ctx* c) {
         const int pairs = (c->mloc + 1) / 2;
         const int grid = std::max(1, std::min(pairs, per_sm * c->num_sms));
         c->construct_grid = grid;
+        c->construct_desc = "k_construct_roulette_pair<" + std::to_string(c->NV) + "> grid=" +
+                            std::to_string(grid) + " per_sm=" + std::to_string(per_sm) +
+                            " smem=" + std::to_string(smem);
         if (std::getenv("ACO_DEBUG"))
-            std::fprintf(stderr, "construct(pair): NV=%d smem=%zu per_sm=%d grid=%d\n", c->NV, smem,
-                         per_sm, grid);
+            std::fprintf(stderr, "construct: %s\n", c->construct_desc.c_str());
         fn<<<grid, 32, smem, c->stream>>>(p);
         check_launch(c, "k_construct_roulette_pair");
     } else if (c->cfg.selection == ACO_SEL_ROULETTE) {
@@ -357,9 +360,13 @@ void launch_construct(aco_gpu_ctx* c) {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem));
         const int grid = std::max(1, std::min(c->mloc, per_sm * c->num_sms));
         c->construct_grid = grid;
+        c->construct_desc = std::string("k_construct_roulette<") +
+                            (c->stream_kind == ACO_STREAM_FP64 ? "double," : "float,") +
+                            std::to_string(c->NV) + "," + std::to_string(c->MAXR) + "> grid=" +
+                            std::to_string(grid) + " per_sm=" + std::to_string(per_sm) +
+                            " smem=" + std::to_string(smem) + " row=" + std::to_string(c->PW);
         if (std::getenv("ACO_DEBUG"))
-            std::fprintf(stderr, "construct: NV=%d MAXR=%d smem=%zu per_sm=%d grid=%d\n", c->NV,
-                         c->MAXR, smem, per_sm, grid);
+            std::fprintf(stderr, "construct: %s\n", c->construct_desc.c_str());
         fn<<<grid, 32, smem, c->stream>>>(p);
         check_launch(c, "k_construct_roulette");
     } else if (c->cfg.selection == ACO_SEL_NN) {
@@ -367,12 +374,14 @@ void launch_construct(aco_gpu_ctx* c) {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_construct_nn, 32, smem1));
         const int grid = std::max(1, std::min(c->mloc, per_sm * c->num_sms));
         c->construct_grid = grid;
+        c->construct_desc = "k_construct_nn grid=" + std::to_string(grid);
         k_construct_nn<<<grid, 32, smem1, c->stream>>>(p);
         check_launch(c, "k_construct_nn");
     } else {
         const size_t smem4 = smem1 * 4;
         const int grid = std::max(1, (c->mloc + 3) / 4);
         c->construct_grid = grid;
+        c->construct_desc = "k_construct_data_parallel grid=" + std::to_string(grid);
         k_construct_data_parallel<<<grid, 128, smem4, c->stream>>>(p);
         check_launch(c, "k_construct_data_parallel");
     }
@@ -782,6 +791,17 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
 const char* aco_gpu_last_error(const aco_gpu_ctx* c) { return c ? c->err.c_str() : g_host_err.c_str(); }
 
 int64_t aco_gpu_launch_count(const aco_gpu_ctx* c) { return c ? c->launches : 0; }
+
+int32_t aco_gpu_describe(const aco_gpu_ctx* c, char* buf, int32_t len) {
+    if (!c) return 0;
+    const std::string& d = c->construct_desc;
+    if (buf && len > 0) {
+        const size_t k = std::min(d.size(), static_cast<size_t>(len - 1));
+        std::memcpy(buf, d.data(), k);
+        buf[k] = 0;
+    }
+    return static_cast<int32_t>(d.size());
+}
 
 void* aco_gpu_stream(aco_gpu_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
 
