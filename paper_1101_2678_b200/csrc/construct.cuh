@@ -46,6 +46,9 @@
 #ifndef ACO_ROW_SRC
 #define ACO_ROW_SRC 0 // fp32 single-round roulette: 0 = TMA row staging, 1 = L1-allocating LDG
 #endif
+#ifndef ACO_GROUPWALK
+#define ACO_GROUPWALK 1 // fp32 single-round roulette: 1 = group walk, 0 = quad-scan walk
+#endif
 #ifndef ACO_TIMING
 #define ACO_TIMING 0 // per-phase clock64() accounting into ConstructParams::timing
 #endif
@@ -461,6 +464,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
     constexpr int D1 = ceil_log2<GE>() + ceil_log2<NG>();
     constexpr bool F32 = sizeof(WT) == 4;
     constexpr bool kLDG = (ACO_ROW_SRC == 1) && F32 && MAXR == 1; // rows via L1, not smem
+    constexpr bool kGroupWalk = (ACO_GROUPWALK == 1) && F32 && MAXR == 1 && !kLDG;
     static_assert(GE <= 32 && 32 % GE == 0, "a group's bits live in one window word");
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -534,8 +538,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
 
             AT incl[MAXR];
             AT rtot[MAXR];
-            WT gsr[NG];
-            uint32_t win0[NWIN];
+            WT gsr[NG]; // MAXR == 1: lane-local inclusive prefix of the group sums
             AT T = AT(0);
 #pragma unroll
             for (int r = 0; r < MAXR; ++r) {
@@ -580,11 +583,10 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                         else gs[g] = tree_sum<WT, GE>(x);
                         if constexpr (MAXR > 1) gsum[(r * NG + g) * 32 + lane] = gs[g];
                     }
-                    if constexpr (MAXR == 1) {
+                    if constexpr (MAXR == 1) { // lane-local inclusive group prefixes
+                        gsr[0] = gs[0];
 #pragma unroll
-                        for (int g = 0; g < NG; ++g) gsr[g] = gs[g];
-#pragma unroll
-                        for (int i = 0; i < NWIN; ++i) win0[i] = win[i];
+                        for (int g = 1; g < NG; ++g) gsr[g] = gsr[g - 1] + gs[g];
                     }
                     AT d = static_cast<AT>(tree_sum<WT, NG>(gs));
                     TICK(0);
@@ -627,79 +629,147 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                         }
                     }
                 }
-                // crossing lane L of round rs, then a cooperative walk over L's
-                // chunk: lane k takes quad k (4 consecutive cities), quad sums are
-                // scanned across the warp, and the lane holding the crossing quad
-                // walks its 4 cities.
-                const unsigned lb = __ballot_sync(kFull, rs >= 0 && base + my > t);
                 int J = -1;        // candidate city (global index), valid in lane Q
                 bool cert = false; // its certification
-                int Q = -1;
-                if (lb) {
-                    const int L = __ffs(lb) - 1;
-                    const AT myprev = __shfl_sync(kFull, my, L == 0 ? 0 : L - 1);
-                    const AT exclL = base + (L == 0 ? AT(0) : myprev);
-                    constexpr int NQT = C / 4; // quads per chunk
-                    const int cbaseL = rs * 32 * C + L * C;
-                    // all lanes load (lanes >= NQT re-read quad 0 and drop it)
-                    const int ql = lane < NQT ? lane : 0;
-                    AT xv[4];
-                    if constexpr (F32) {
-                        const float4* qp = reinterpret_cast<const float4*>(
-                            rowsrc + rs * kLP * C + (ql * kLP + L) * 4);
-                        float4 v;
-                        if constexpr (kLDG) v = __ldg(qp);
-                        else v = *qp;
-                        xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
-                    } else {
-                        const double2 v0 = *reinterpret_cast<const double2*>(
-                            buf + rs * kLP * C + ((2 * ql) * kLP + L) * 2);
-                        const double2 v1 = *reinterpret_cast<const double2*>(
-                            buf + rs * kLP * C + ((2 * ql + 1) * kLP + L) * 2);
-                        xv[0] = v0.x; xv[1] = v0.y; xv[2] = v1.x; xv[3] = v1.y;
-                    }
-                    {
-                        const int c0 = cbaseL + 4 * ql;
-                        uint32_t bits4 =
-                            __funnelshift_r(tabu[c0 >> 5], tabu[(c0 >> 5) + 1], c0 & 31);
-                        if (lane >= NQT) bits4 = 0xFu;
+                if constexpr (kGroupWalk) {
+                    // Group walk (MAXR == 1, fp32): every lane locates the
+                    // crossing GROUP of its own chunk from its group prefixes
+                    // (no extra shared reads); lane L's group G and exclusive
+                    // base are broadcast, and lanes 0..3 each take one 4-city
+                    // quad of that group: quad prefixes by three parallel
+                    // shuffles, the first crossing city by one ballot.
+                    const AT exo = __shfl_up_sync(kFull, incl[0], 1);
+                    const AT excl_own = lane == 0 ? AT(0) : exo;
+                    const unsigned lb = __ballot_sync(kFull, incl[0] > t);
+                    // crossing group of the own chunk: the number of group
+                    // prefixes <= t - excl_own (a wrong pick in a rounding tie
+                    // only fails certification); its exclusive base.
+                    const AT tl = t - excl_own;
+                    int Gown = 0;
+                    AT gb = AT(0);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            if ((bits4 >> q) & 1u) xv[q] = AT(0);
+                    for (int g = 0; g < NG; ++g) {
+                        const bool below = gsr[g] <= tl;
+                        Gown += below ? 1 : 0;
+                        gb = below ? gsr[g] : gb;
                     }
-                    const AT qs = (xv[0] + xv[1]) + (xv[2] + xv[3]);
-                    AT qi = qs;
-                    if constexpr (F32) {
-                        qi = warp_inclusive_scan(qi);
-                    } else {
-#pragma unroll
-                        for (int off = 1; off < 32; off <<= 1) {
-                            const AT y = __shfl_up_sync(kFull, qi, off);
-                            if (lane >= off) qi += y;
+                    const AT bG = excl_own + gb;
+                    if (lb) {
+                        const int L = __ffs(lb) - 1;
+                        const int G = __shfl_sync(kFull, Gown, L);
+                        const AT baseG = __shfl_sync(kFull, bG, L);
+                        if (G < NG) {
+                            const int k = lane & 3;
+                            const int tv = G * GV + k;
+                            const int c0 = L * C + tv * 4; // first city of the quad
+                            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                            uint32_t bits4 = 0xFu;
+                            if (tv < NV) {
+                                v = reinterpret_cast<const float4*>(buf)[tv * kLP + L];
+                                bits4 = __funnelshift_r(tabu[c0 >> 5], tabu[(c0 >> 5) + 1], c0 & 31);
+                            }
+                            AT x0 = (bits4 & 1u) ? AT(0) : v.x;
+                            AT x1 = (bits4 & 2u) ? AT(0) : v.y;
+                            AT x2 = (bits4 & 4u) ? AT(0) : v.z;
+                            AT x3 = (bits4 & 8u) ? AT(0) : v.w;
+                            const AT a1 = x0 + x1;
+                            const AT a2 = a1 + x2;
+                            const AT a3 = a2 + x3;
+                            const AT s1 = __shfl_up_sync(kFull, a3, 1, 4);
+                            const AT s2 = __shfl_up_sync(kFull, a3, 2, 4);
+                            const AT s3 = __shfl_up_sync(kFull, a3, 3, 4);
+                            const AT ex = (k >= 1 ? s1 : AT(0)) + ((k >= 2 ? s2 : AT(0)) + (k >= 3 ? s3 : AT(0)));
+                            const AT kb = baseG + ex;
+                            const AT p0 = kb + x0, p1 = kb + a1, p2 = kb + a2, p3 = kb + a3;
+                            int E = -1;
+                            AT Pj32 = AT(0), Pp32 = AT(0);
+                            // first q with x_q > 0 and P_q > t (descending so the lowest wins)
+                            if (x3 > AT(0) && p3 > t) { E = 3; Pj32 = p3; Pp32 = p2; }
+                            if (x2 > AT(0) && p2 > t) { E = 2; Pj32 = p2; Pp32 = p1; }
+                            if (x1 > AT(0) && p1 > t) { E = 1; Pj32 = p1; Pp32 = p0; }
+                            if (x0 > AT(0) && p0 > t) { E = 0; Pj32 = p0; Pp32 = kb; }
+                            const unsigned qb = __ballot_sync(kFull, lane < 4 && E >= 0);
+                            const bool mine = qb != 0u && lane == __ffs(qb) - 1;
+                            const double Pj = static_cast<double>(Pj32);
+                            const double Pprev = static_cast<double>(Pp32);
+                            const int Jc = c0 + E;
+                            J = mine ? Jc : -1;
+                            cert = mine && (Pj * lo_f > A) && (Pprev + e_rel * Pj < B) && Jc < n;
                         }
                     }
-                    const AT qe = __shfl_up_sync(kFull, qi, 1);
-                    const unsigned qb = __ballot_sync(kFull, lane < NQT && exclL + qi > t);
-                    Q = __ffs(qb) - 1;
-                    // every lane walks its own quad; only lane Q's result is kept
-                    AT ea = exclL + (lane == 0 ? AT(0) : qe);
-                    AT Pj32 = AT(0), Pp32 = AT(0);
-                    int E = -1;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const AT na = ea + xv[q];
-                        const bool hit = (E < 0) && (xv[q] > AT(0)) && (na > t);
-                        Pj32 = hit ? na : Pj32;
-                        Pp32 = hit ? ea : Pp32;
-                        E = hit ? q : E;
-                        ea = na;
+                } else {
+                    // crossing lane L of round rs, then a cooperative walk over L's
+                    // chunk: lane k takes quad k (4 consecutive cities), quad sums are
+                    // scanned across the warp, and the lane holding the crossing quad
+                    // walks its 4 cities.
+                    const unsigned lb = __ballot_sync(kFull, rs >= 0 && base + my > t);
+                    int Q = -1;
+                    if (lb) {
+                        const int L = __ffs(lb) - 1;
+                        const AT myprev = __shfl_sync(kFull, my, L == 0 ? 0 : L - 1);
+                        const AT exclL = base + (L == 0 ? AT(0) : myprev);
+                        constexpr int NQT = C / 4; // quads per chunk
+                        const int cbaseL = rs * 32 * C + L * C;
+                        // all lanes load (lanes >= NQT re-read quad 0 and drop it)
+                        const int ql = lane < NQT ? lane : 0;
+                        AT xv[4];
+                        if constexpr (F32) {
+                            const float4* qp = reinterpret_cast<const float4*>(
+                                rowsrc + rs * kLP * C + (ql * kLP + L) * 4);
+                            float4 v;
+                            if constexpr (kLDG) v = __ldg(qp);
+                            else v = *qp;
+                            xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
+                        } else {
+                            const double2 v0 = *reinterpret_cast<const double2*>(
+                                buf + rs * kLP * C + ((2 * ql) * kLP + L) * 2);
+                            const double2 v1 = *reinterpret_cast<const double2*>(
+                                buf + rs * kLP * C + ((2 * ql + 1) * kLP + L) * 2);
+                            xv[0] = v0.x; xv[1] = v0.y; xv[2] = v1.x; xv[3] = v1.y;
+                        }
+                        {
+                            const int c0 = cbaseL + 4 * ql;
+                            uint32_t bits4 =
+                                __funnelshift_r(tabu[c0 >> 5], tabu[(c0 >> 5) + 1], c0 & 31);
+                            if (lane >= NQT) bits4 = 0xFu;
+    #pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                if ((bits4 >> q) & 1u) xv[q] = AT(0);
+                        }
+                        const AT qs = (xv[0] + xv[1]) + (xv[2] + xv[3]);
+                        AT qi = qs;
+                        if constexpr (F32) {
+                            qi = warp_inclusive_scan(qi);
+                        } else {
+    #pragma unroll
+                            for (int off = 1; off < 32; off <<= 1) {
+                                const AT y = __shfl_up_sync(kFull, qi, off);
+                                if (lane >= off) qi += y;
+                            }
+                        }
+                        const AT qe = __shfl_up_sync(kFull, qi, 1);
+                        const unsigned qb = __ballot_sync(kFull, lane < NQT && exclL + qi > t);
+                        Q = __ffs(qb) - 1;
+                        // every lane walks its own quad; only lane Q's result is kept
+                        AT ea = exclL + (lane == 0 ? AT(0) : qe);
+                        AT Pj32 = AT(0), Pp32 = AT(0);
+                        int E = -1;
+    #pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const AT na = ea + xv[q];
+                            const bool hit = (E < 0) && (xv[q] > AT(0)) && (na > t);
+                            Pj32 = hit ? na : Pj32;
+                            Pp32 = hit ? ea : Pp32;
+                            E = hit ? q : E;
+                            ea = na;
+                        }
+                        const double Pj = static_cast<double>(Pj32);
+                        const double Pprev = static_cast<double>(Pp32);
+                        const int Jc = cbaseL + 4 * lane + E;
+                        const bool mine = (lane == Q) && (E >= 0);
+                        J = mine ? Jc : -1;
+                        cert = mine && (Pj * lo_f > A) && (Pprev + e_rel * Pj < B) && Jc < n;
                     }
-                    const double Pj = static_cast<double>(Pj32);
-                    const double Pprev = static_cast<double>(Pp32);
-                    const int Jc = cbaseL + 4 * lane + E;
-                    const bool mine = (lane == Q) && (E >= 0);
-                    J = mine ? Jc : -1;
-                    cert = mine && (Pj * lo_f > A) && (Pprev + e_rel * Pj < B) && Jc < n;
                 }
                 TICK(2);
                 // speculative refill, issued by the certifying lane itself: every

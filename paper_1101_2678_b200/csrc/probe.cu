@@ -9,12 +9,14 @@
 
 namespace {
 
+template <int CG>
 __global__ void k_read(const float4* __restrict__ p, size_t n4, int reps, float* sink) {
     float acc = 0.f;
     for (int r = 0; r < reps; ++r) {
+        // CG = 1: ld.global.cg (cached in L2 only), so no repetition can hit in L1
         for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
              i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-            const float4 v = __ldg(p + i);
+            const float4 v = CG ? __ldcg(p + i) : __ldg(p + i);
             acc += v.x + v.y + v.z + v.w;
         }
     }
@@ -23,8 +25,9 @@ __global__ void k_read(const float4* __restrict__ p, size_t n4, int reps, float*
 
 } // namespace
 
-extern "C" int aco_probe_read_bw(int device, size_t bytes, int reps, int iters, double* gbps,
-                                 double* ms_out) {
+extern "C" int aco_probe_read_bw_mode(int device, size_t bytes, int reps, int iters, int cg,
+                                      double* gbps, double* ms_out) {
+    auto kern = cg ? k_read<1> : k_read<0>;
     if (cudaSetDevice(device) != cudaSuccess) return 1;
     float4* buf = nullptr;
     float* sink = nullptr;
@@ -37,12 +40,12 @@ extern "C" int aco_probe_read_bw(int device, size_t bytes, int reps, int iters, 
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    k_read<<<sms * 8, 512>>>(buf, n4, 1, sink); // warm (L2-resident when it fits)
+    kern<<<sms * 8, 512>>>(buf, n4, 1, sink); // warm (L2-resident when it fits)
     cudaDeviceSynchronize();
     double best = 1e30;
     for (int it = 0; it < iters; ++it) {
         cudaEventRecord(a);
-        k_read<<<sms * 8, 512>>>(buf, n4, reps, sink);
+        kern<<<sms * 8, 512>>>(buf, n4, reps, sink);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms = 0.f;
@@ -56,6 +59,11 @@ extern "C" int aco_probe_read_bw(int device, size_t bytes, int reps, int iters, 
     cudaFree(buf);
     cudaFree(sink);
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+extern "C" int aco_probe_read_bw(int device, size_t bytes, int reps, int iters, double* gbps,
+                                 double* ms_out) {
+    return aco_probe_read_bw_mode(device, bytes, reps, iters, 0, gbps, ms_out);
 }
 
 // ---- dependent-chain latency probes (cycles per op, one warp) -------------
@@ -100,4 +108,190 @@ extern "C" int aco_probe_latency(int device, int op, int iters, double* cycles_p
     *cycles_per_op = static_cast<double>(h) / (16.0 * iters);
     cudaFree(out); cudaFree(outf); cudaFree(cyc);
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+// ---- row-staging probe: how fast can one-warp CTAs move rows into registers?
+// Each CTA (one warp) processes `steps` rows of `row_bytes`, the next row index
+// depending on the data of the current one (the construction's dependence).
+//   mode 0: TMA (cp.async.bulk) into smem, mbarrier wait, LDS.128 + sum
+//   mode 1: same, but the next row's TMA is issued before the reads (2 buffers)
+//   mode 2: LDG.128 (ld.global.nc) straight into registers + sum
+//   mode 3: LDS.128 + sum of a resident smem row (no refill)
+//   mode 4: LDG.128 with L1::no_allocate
+namespace {
+__device__ __forceinline__ uint32_t pr_smem(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void pr_tma(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(pr_smem(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            pr_smem(dst)),
+        "l"(src), "r"(bytes), "r"(pr_smem(bar))
+        : "memory");
+}
+__device__ __forceinline__ void pr_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}" ::"r"(
+            pr_smem(bar)),
+        "r"(phase)
+        : "memory");
+}
+template <int MODE, int NV>
+__global__ void __launch_bounds__(32, MODE == 6 ? 8 : 17) k_stage(const float4* __restrict__ rows, int nrows, int steps,
+                                                  float* sink) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
+    float4* buf0 = reinterpret_cast<float4*>(sm + 128);
+    float4* buf1 = buf0 + 32 * NV;
+    const int lane = threadIdx.x;
+    constexpr uint32_t RB = 32 * NV * 16;
+    if (lane == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(pr_smem(bar)));
+    __syncwarp();
+    uint32_t phase = 0;
+    uint32_t h = blockIdx.x * 2654435761u + 12345u;
+    int idx = h % nrows;
+    float acc = 0.f;
+    if (MODE == 1 || MODE == 3) {
+        if (lane == 0) pr_tma(buf0, rows + static_cast<size_t>(idx) * 32 * NV, RB, bar);
+        pr_wait(bar, phase);
+        phase ^= 1;
+    }
+    int cb = 0;
+    for (int s = 0; s < steps; ++s) {
+        h = h * 1664525u + 1013904223u;
+        float4* cur = (MODE == 1 && cb) ? buf1 : buf0;
+        if (MODE == 0) {
+            __syncwarp();
+            if (lane == 0) pr_tma(buf0, rows + static_cast<size_t>(idx) * 32 * NV, RB, bar);
+            pr_wait(bar, phase);
+            phase ^= 1;
+        }
+        if (MODE == 5) { // the same row as 4 bulk copies (one per lane 0..3)
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(pr_smem(bar)),
+                             "r"(RB)
+                             : "memory");
+            __syncwarp();
+            if (lane < 4) {
+                const uint32_t q = RB / 4;
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        pr_smem(reinterpret_cast<char*>(buf0) + lane * q)),
+                    "l"(reinterpret_cast<const char*>(rows + static_cast<size_t>(idx) * 32 * NV) + lane * q),
+                    "r"(q), "r"(pr_smem(bar))
+                    : "memory");
+            }
+            pr_wait(bar, phase);
+            phase ^= 1;
+        }
+        if (MODE == 6) { // LDG, two rows in flight (data-independent index)
+            float4 a[NV], b[NV];
+            const float4* g0 = rows + static_cast<size_t>(idx) * 32 * NV;
+#pragma unroll
+            for (int t = 0; t < NV; ++t) a[t] = __ldg(g0 + t * 32 + lane);
+            for (; s + 1 < steps; s += 2) {
+                h = h * 1664525u + 1013904223u;
+                const float4* g1 = rows + static_cast<size_t>((h >> 8) % nrows) * 32 * NV;
+#pragma unroll
+                for (int t = 0; t < NV; ++t) b[t] = __ldg(g1 + t * 32 + lane);
+                float s0 = 0.f;
+#pragma unroll
+                for (int t = 0; t < NV; ++t) s0 += (a[t].x + a[t].y) + (a[t].z + a[t].w);
+                h = h * 1664525u + 1013904223u;
+                const float4* g2 = rows + static_cast<size_t>((h >> 8) % nrows) * 32 * NV;
+#pragma unroll
+                for (int t = 0; t < NV; ++t) a[t] = __ldg(g2 + t * 32 + lane);
+#pragma unroll
+                for (int t = 0; t < NV; ++t) s0 += (b[t].x + b[t].y) + (b[t].z + b[t].w);
+                acc += s0;
+            }
+            break;
+        }
+        float sum = 0.f;
+        const float4* g = rows + static_cast<size_t>(idx) * 32 * NV;
+        if (MODE == 1) { // next row index is data-independent here (best case)
+            const int nidx = (h >> 8) % nrows;
+            __syncwarp();
+            if (lane == 0) pr_tma(cb ? buf0 : buf1, rows + static_cast<size_t>(nidx) * 32 * NV, RB, bar);
+            idx = nidx;
+        }
+#pragma unroll
+        for (int t = 0; t < NV; ++t) {
+            float4 v;
+            if (MODE == 2) v = __ldg(g + t * 32 + lane);
+            else if (MODE == 4) {
+                asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                             : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                             : "l"(g + t * 32 + lane));
+            } else if (MODE == 3) {
+                asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                             : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                             : "r"(pr_smem(cur + t * 32 + lane)));
+            } else v = cur[t * 32 + lane];
+            sum += (v.x + v.y) + (v.z + v.w);
+        }
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        acc += sum;
+        if (MODE == 1) {
+            pr_wait(bar, phase);
+            phase ^= 1;
+            cb ^= 1;
+        } else {
+            idx = static_cast<int>((h >> 8) % nrows) + static_cast<int>(sum); // data-dependent
+            if (idx >= nrows) idx = 0;
+        }
+    }
+    if (acc == 1234.5f) *sink = acc;
+}
+template <int MODE>
+int run_stage(int device, int warps_per_sm, int steps, double* gbps, double* ms_out) {
+    constexpr int NV = 19;
+    constexpr int RB = 32 * NV * 16;
+    const int nrows = 2392;
+    float4* rows = nullptr;
+    float* sink = nullptr;
+    if (cudaMalloc(&rows, static_cast<size_t>(nrows) * RB) != cudaSuccess) return 2;
+    cudaMalloc(&sink, 4);
+    cudaMemset(rows, 0, static_cast<size_t>(nrows) * RB);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int smem = 128 + RB * ((MODE == 1) ? 2 : 1);
+    cudaFuncSetAttribute(k_stage<MODE, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int grid = sms * warps_per_sm;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    k_stage<MODE, NV><<<grid, 32, smem>>>(rows, nrows, 50, sink);
+    cudaDeviceSynchronize();
+    cudaEventRecord(a);
+    k_stage<MODE, NV><<<grid, 32, smem>>>(rows, nrows, steps, sink);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    *ms_out = ms;
+    *gbps = static_cast<double>(grid) * steps * RB / (ms * 1e-3) / 1e9;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(rows);
+    cudaFree(sink);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+} // namespace
+
+extern "C" int aco_probe_stage(int device, int mode, int warps_per_sm, int steps, double* gbps,
+                               double* ms) {
+    cudaSetDevice(device);
+    switch (mode) {
+    case 0: return run_stage<0>(device, warps_per_sm, steps, gbps, ms);
+    case 1: return run_stage<1>(device, warps_per_sm, steps, gbps, ms);
+    case 2: return run_stage<2>(device, warps_per_sm, steps, gbps, ms);
+    case 3: return run_stage<3>(device, warps_per_sm, steps, gbps, ms);
+    case 4: return run_stage<4>(device, warps_per_sm, steps, gbps, ms);
+    case 5: return run_stage<5>(device, warps_per_sm, steps, gbps, ms);
+    default: return run_stage<6>(device, warps_per_sm, steps, gbps, ms);
+    }
 }
