@@ -87,6 +87,9 @@ def main():
         ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
         per = collections.defaultdict(list)
         for r in rows[1:]:
+            # bench.py's roofline probes and its L2-flush fill are not part of the step
+            if "<unnamed>::k_" in r[ik] or "FillFunctor" in r[ik]:
+                continue
             v = float(r[iv].replace(",", ""))
             v = v / 1e3 if r[iu] in ("ns", "nsecond") else (v * 1e3 if r[iu] in ("ms", "msecond") else v)
             per[r[ik].split("(")[0]].append(v)  # usecond
