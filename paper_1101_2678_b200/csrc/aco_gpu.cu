@@ -281,6 +281,15 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
     rp.alpha = c->cfg.alpha;
     rp.keep = 1.0 - c->cfg.rho; // pheromone.hpp:179
     const size_t smem = static_cast<size_t>(c->P64) * sizeof(double);
+    const size_t wsmem = smem + 32 * sizeof(double);
+    if (mode == MODE_GATHER && wsmem <= 32 * 1024) { // one warp per row
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_gather_warp, 32, wsmem));
+        const int grid = std::max(1, std::min(c->n, per_sm * c->num_sms));
+        k_rows_gather_warp<<<grid, 32, wsmem, c->stream>>>(rp);
+        check_launch(c, "k_rows_gather_warp");
+        return;
+    }
     const int grid = std::min(c->n, c->num_sms * 8);
     if (smem > 48 * 1024) {
         CK(cudaFuncSetAttribute(k_rows<MODE_CHOICE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

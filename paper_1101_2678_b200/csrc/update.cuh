@@ -167,6 +167,41 @@ struct RowParams {
     double alpha, keep;
 };
 
+// Write one row of the permuted streamed layout (stream_pos) from the natural
+// row in shared memory: one V-wide vector slot (V consecutive cities of one
+// lane chunk, or a pad slot) per iteration, so the index arithmetic is two
+// divisions per vector instead of three per city.  V = 4: fp32 scaled by
+// 2^sc; V = 2: fp64 as is.
+template <int V, typename OT>
+__device__ __forceinline__ void write_stream_row(OT* __restrict__ crow, const double* rowbuf, int n,
+                                                 int PW, int C, int LA, int sc, int tid,
+                                                 int nthreads) {
+    const int LP = LA + 1, NVL = C / V, RS = LP * NVL; // vector slots per round
+    const int nslots = PW / V;
+    for (int s = tid; s < nslots; s += nthreads) {
+        const int r = s / RS, rem = s - r * RS;
+        const int t = rem / LP, l = rem - t * LP;
+        const int c0 = r * LA * C + l * C + t * V;
+        if constexpr (V == 4) {
+            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (l < LA) {
+                if (c0 + 0 < n) o.x = __double2float_rn(scalbn(rowbuf[c0 + 0], sc));
+                if (c0 + 1 < n) o.y = __double2float_rn(scalbn(rowbuf[c0 + 1], sc));
+                if (c0 + 2 < n) o.z = __double2float_rn(scalbn(rowbuf[c0 + 2], sc));
+                if (c0 + 3 < n) o.w = __double2float_rn(scalbn(rowbuf[c0 + 3], sc));
+            }
+            reinterpret_cast<float4*>(crow)[s] = o;
+        } else {
+            double2 o = make_double2(0.0, 0.0);
+            if (l < LA) {
+                if (c0 + 0 < n) o.x = rowbuf[c0 + 0];
+                if (c0 + 1 < n) o.y = rowbuf[c0 + 1];
+            }
+            reinterpret_cast<double2*>(crow)[s] = o;
+        }
+    }
+}
+
 __device__ __forceinline__ double tau_pow(double t, double alpha) {
     if (alpha == 1.0) return t;  // pow(x, 1) == x exactly (SURVEY [E1])
     if (alpha == 0.0) return 1.0; // pow(x, 0) == 1 exactly
@@ -252,20 +287,134 @@ __global__ void __launch_bounds__(256) k_rows(RowParams p) {
             // Exact power-of-two scale: row max -> [2^100, 2^101).
             const int sc = rmx > 0.0 ? 100 - ilogb(rmx) : 0;
             if (tid == 0) p.scale_exp[i] = sc;
-            float* crow = p.choice32 + static_cast<size_t>(i) * p.PW;
-            for (int q = tid; q < p.PW; q += blockDim.x) {
-                const int c = stream_city(q, p.C, 4, p.LA);
-                crow[q] = c < n ? __double2float_rn(scalbn(rowbuf[c], sc)) : 0.0f; // pads 0
-            }
+            write_stream_row<4>(p.choice32 + static_cast<size_t>(i) * p.PW, rowbuf, n, p.PW, p.C,
+                                p.LA, sc, tid, blockDim.x); // pads 0
         }
         if (p.choice_perm64) {
-            double* crow = p.choice_perm64 + static_cast<size_t>(i) * p.PW;
-            for (int q = tid; q < p.PW; q += blockDim.x) {
-                const int c = stream_city(q, p.C, 2, p.LA);
-                crow[q] = c < n ? rowbuf[c] : 0.0;
-            }
+            write_stream_row<2>(p.choice_perm64 + static_cast<size_t>(i) * p.PW, rowbuf, n, p.PW,
+                                p.C, p.LA, 0, tid, blockDim.x);
         }
         __syncthreads();
+    }
+}
+
+// MODE_GATHER with one WARP per pheromone row (n small enough that a row of
+// doubles fits a warp's shared-memory slice).  The CTA-per-row k_rows<GATHER>
+// makes each of its 8 warps read the whole contribution stream of the row
+// (warp w owns columns c % 8 == w); here one warp reads it once, in
+// ascending global ant order, 16 ants (32 contributions: pred, succ) per
+// chunk, four chunks loaded ahead.  Equal columns inside a chunk are found
+// with __match_any_sync and folded by their lowest lane in lane (= ant)
+// order from a per-warp staging array, so every column is the same
+// sequential fold from 0.0 as gather_cell (pheromone.hpp:133-148).  The
+// epilogue (tau update, choice, scaled fp32 stream) is k_rows' own, per warp.
+__global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
+    extern __shared__ double wsm[]; // rowbuf[P64] + stage[32]
+    double* rowbuf = wsm;
+    double* stage = wsm + p.P64;
+    const int lane = threadIdx.x & 31;
+    const int n = p.n;
+    constexpr int AHEAD = 8;
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        double* trow = p.tau + static_cast<size_t>(i) * p.P64;
+        for (int j = lane; j < n; j += 32) rowbuf[j] = 0.0;
+        __syncwarp();
+        for (int g = 0; g < p.shards; ++g) {
+            const int kbeg = g * p.S;
+            const int cnt = min(p.S, p.m - kbeg);
+            const int32_t* sc = p.succ + (static_cast<size_t>(g) * n + i) * p.S;
+            const int32_t* pc = p.pred + (static_cast<size_t>(g) * n + i) * p.S;
+            const double* wv = p.inv + static_cast<size_t>(g) * p.S;
+            for (int k0 = 0; k0 < cnt; k0 += 16 * AHEAD) {
+                int col[AHEAD];
+                double w[AHEAD];
+#pragma unroll
+                for (int u = 0; u < AHEAD; ++u) {
+                    const int k = k0 + 16 * u + (lane >> 1);
+                    col[u] = -1;
+                    w[u] = 0.0;
+                    if (k < cnt) {
+                        col[u] = __ldg((lane & 1) ? sc + k : pc + k);
+                        w[u] = __ldg(wv + k);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < AHEAD; ++u) {
+                    const int cu = col[u];
+                    const unsigned grp = __match_any_sync(kFull, cu);
+                    const bool lead = cu >= 0 && lane == __ffs(grp) - 1;
+                    if (!__any_sync(kFull, cu >= 0 && __popc(grp) > 1)) {
+                        // all columns distinct: one add each, in parallel
+                        if (cu >= 0) rowbuf[cu] = __dadd_rn(rowbuf[cu], w[u]);
+                    } else {
+                        // every lane folds the 32 staged values of its group in
+                        // lane (= ant) order; only group leaders keep the result
+                        stage[lane] = w[u];
+                        __syncwarp();
+                        double acc = lead ? rowbuf[cu] : 0.0;
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) {
+                            const double v = stage[q];
+                            acc = ((grp >> q) & 1u) ? __dadd_rn(acc, v) : acc;
+                        }
+                        if (lead) rowbuf[cu] = acc;
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        double mx = 0.0;
+        const int32_t* drow = p.dist + static_cast<size_t>(i) * p.P64;
+        const double* erow = p.etab ? p.etab + static_cast<size_t>(i) * p.P64 : nullptr;
+        // batches of EB columns per lane: all tau / dist loads, then all
+        // eta^beta gathers, then the arithmetic (one warp per row has no other
+        // latency hiding than these independent loads)
+        constexpr int EB = 8;
+        for (int j0 = 0; j0 < n; j0 += 32 * EB) {
+            double tv[EB], eb[EB];
+            int dv[EB];
+#pragma unroll
+            for (int u = 0; u < EB; ++u) {
+                const int j = j0 + 32 * u + lane;
+                tv[u] = j < n ? trow[j] : 0.0;
+                dv[u] = (j < n && !erow) ? __ldg(drow + j) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < EB; ++u) {
+                const int j = j0 + 32 * u + lane;
+                eb[u] = j < n ? (erow ? __ldg(erow + j) : __ldg(p.lut + dv[u])) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < EB; ++u) {
+                const int j = j0 + 32 * u + lane;
+                if (j < n) {
+                    const double t = __dadd_rn(__dmul_rn(tv[u], p.keep), rowbuf[j]);
+                    trow[j] = t;
+                    const double c = (j == i) ? 0.0 : __dmul_rn(tau_pow(t, p.alpha), eb[u]);
+                    p.choice64[static_cast<size_t>(i) * p.P64 + j] = c;
+                    rowbuf[j] = c;
+                    mx = fmax(mx, c);
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, off));
+        __syncwarp();
+        if (p.choice_nn)
+            for (int q = lane; q < p.nn; q += 32)
+                p.choice_nn[static_cast<size_t>(i) * p.nn + q] =
+                    rowbuf[p.nn_lists[static_cast<size_t>(i) * p.nn + q]];
+        if (p.choice32) {
+            const int sc = mx > 0.0 ? 100 - ilogb(mx) : 0;
+            if (lane == 0) p.scale_exp[i] = sc;
+            write_stream_row<4>(p.choice32 + static_cast<size_t>(i) * p.PW, rowbuf, n, p.PW, p.C,
+                                p.LA, sc, lane, 32);
+        }
+        if (p.choice_perm64) {
+            write_stream_row<2>(p.choice_perm64 + static_cast<size_t>(i) * p.PW, rowbuf, n, p.PW,
+                                p.C, p.LA, 0, lane, 32);
+        }
+        __syncwarp();
     }
 }
 
