@@ -718,10 +718,14 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         CK(cudaMemset(c->d_tours, 0, ml * (n + 1) * sizeof(int32_t)));
         CK(cudaMalloc(&c->d_len, ml * sizeof(int64_t)));
         CK(cudaMalloc(&c->d_inv, static_cast<size_t>(c->world) * c->S * sizeof(double)));
+        CK(cudaMemset(c->d_inv, 0, static_cast<size_t>(c->world) * c->S * sizeof(double)));
         if (c->cfg.deposit != ACO_DEP_ACCUMULATE) {
+            // zeroed: a shard block not yet exchanged folds +0.0 into column 0
             const size_t sp = static_cast<size_t>(c->world) * n * c->S;
             CK(cudaMalloc(&c->d_succ, sp * sizeof(int32_t)));
             CK(cudaMalloc(&c->d_pred, sp * sizeof(int32_t)));
+            CK(cudaMemset(c->d_succ, 0, sp * sizeof(int32_t)));
+            CK(cudaMemset(c->d_pred, 0, sp * sizeof(int32_t)));
         } else if (c->world > 1) {
             CK(cudaMalloc(&c->d_delta, cells * sizeof(double)));
             CK(cudaMemset(c->d_delta, 0, cells * sizeof(double)));

@@ -1,0 +1,202 @@
+"""Every BASELINE.json workload on one B200: ms per iteration split into
+construction and update, each as an absolute time and as a fraction of its
+roofline, with the reference's CPU Engine timed on the same host in the same
+run (north star "For every workload, report ...").
+
+    python tools/workloads.py [--out gpurun_out/workloads.json] [--quick]
+
+Multi-GPU configurations run as SHARD EMULATION on the one GPU: an engine in
+external-exchange mode (world = G, rank 0, no NCCL) builds exactly rank 0's
+ant shard (m/G ants; the ants are keyed by their global id) and runs the
+replicated update.  Construction and update times are therefore the per-GPU
+device times of a G-GPU run; the NCCL exchange itself cannot be timed on a
+one-GPU box and is reported as bytes moved, its time as a labelled model.
+
+Rooflines:
+  construction (roulette): B_c = m_local*(n-1)*n*4 bytes (one fp32 row per
+      ant-step) over the live-measured L2 row-staging peak;
+  construction (nn):       m_local*(n-1)*(nn*(8+4)) list bytes + one fp64 row
+      (n*8) per argmax-fallback step, over the same L2 peak (the lists are
+      L2-resident; the fallback rows stream from HBM at 10k);
+  update (accumulate):     evaporate 16*n*P + deposit 2*m*n red.f64 (8 B each)
+      + tours 4*m*(n+1) + choice epilogue (8+4+8+4)*n*P, over HBM peak;
+  update (gather):         (8+8+4+8+4)*n*P + 16*m*n + 8*m, over HBM peak.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+
+def l2_and_hbm_peaks(device=0):
+    import bench
+
+    bw = bench.measure_l2_read_bw(device)
+    peaks = bench.load_peaks()
+    return {"l2_gbs": bw["l2_read_gbs"], "l2_rows_gbs": bw["l2_rows_gbs"],
+            "l2_cg_gbs": bw["l2_cg_gbs"],
+            "hbm_gbs": peaks.get("hbm_gbs") or bw["hbm_read_gbs"],
+            "hbm_source": "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs")
+            else "live 2 GiB read (libaco_probe.so)"}
+
+
+def time_engine(aco, torch, prob, n, m, selection, deposit, G, iters, warmup, nn=30):
+    cfg = aco.RunConfig(params=aco.Parameters(m=m, seed=1, nn=nn),
+                        selection=aco.SelectionStrategy(aco.Selection(selection)),
+                        deposit=aco.DepositStrategy(aco.Deposit(deposit)),
+                        world=G, rank=0)
+    eng = aco.Engine(prob, cfg)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    sp = torch.cuda.ExternalStream(eng.stream_handle(), device="cuda")
+    recs = []
+    for i in range(warmup + iters):
+        with torch.cuda.stream(sp):
+            flush.fill_(i & 0xFF)
+        r = eng.run_iteration()
+        if i >= warmup:
+            recs.append(r)
+    torch.cuda.synchronize()
+    out = {
+        "m_local": eng.ant_end - eng.ant_begin,
+        "construct_ms": statistics.median(r.construct_ms for r in recs),
+        "construct_kernel_ms": statistics.median(r.construct_kernel_ms for r in recs),
+        "update_ms": statistics.median(r.update_ms for r in recs),
+        "choice_ms": statistics.median(r.choice_ms for r in recs),
+        "fallback_steps_per_iter": statistics.mean(r.fallbacks for r in recs),
+        "best_length_last": recs[-1].best_length,
+        "kernel": eng.describe(),
+        "iterations": iters,
+    }
+    out["ms_per_iter"] = out["construct_ms"] + out["update_ms"]
+    eng.close()
+    del flush
+    return out
+
+
+def cpu_reference(n, m, selection, deposit, iters, nn=30):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import RefEngine, synth_coords  # cpu baseline leg only
+
+    xs, ys = synth_coords(n)
+    t0 = time.time()
+    eng = RefEngine(xs, ys, m=m, nn=nn, seed=1, selection=selection, deposit=deposit, workers=0)
+    create = time.time() - t0
+    recs = [eng.run_iteration() for _ in range(iters)]
+    return {"construct_ms": statistics.mean(r["construct_ms"] for r in recs),
+            "update_ms": statistics.mean(r["update_ms"] for r in recs),
+            "ms_per_iter": statistics.mean(r["construct_ms"] + r["update_ms"] for r in recs),
+            "cores": eng.workers, "iterations": iters, "create_s": round(create, 2),
+            "kind": "reference (oracle/_ref: proj/include/aco compiled unmodified, -O3)"}
+
+
+def rooflines(res, n, m_total, selection, deposit, nn, peaks):
+    P = (n + 31) // 32 * 32
+    ml = res["m_local"]
+    if selection == 1:
+        b_c = ml * (n - 1) * nn * (8 + 4) + res["fallback_steps_per_iter"] * n * 8
+    else:
+        b_c = ml * (n - 1) * n * 4
+    if deposit == 0:
+        b_u = 16 * n * P + 2 * m_total * n * 8 + 4 * m_total * (n + 1) + 24 * n * P
+    else:
+        b_u = 32 * n * P + 16 * m_total * n + 8 * m_total
+    c_gbs = b_c / (res["construct_kernel_ms"] * 1e-3) / 1e9
+    u_gbs = b_u / (res["update_ms"] * 1e-3) / 1e9
+    return {
+        "construct": {"bytes": int(b_c), "achieved_gbs": round(c_gbs, 1), "bound": "l2",
+                      "peak_gbs": peaks["l2_gbs"], "frac": round(c_gbs / peaks["l2_gbs"], 4)},
+        "update": {"bytes": int(b_u), "achieved_gbs": round(u_gbs, 1), "bound": "hbm",
+                   "peak_gbs": peaks["hbm_gbs"], "frac": round(u_gbs / peaks["hbm_gbs"], 4)},
+    }
+
+
+def exchange_model(n, m_total, G, deposit):
+    """Bytes each GPU sends per iteration over NVLink and a labelled time model
+    (ring all-reduce / all-gather at 700 GB/s bus bandwidth; not measured)."""
+    if G == 1:
+        return None
+    P = (n + 31) // 32 * 32
+    if deposit == 0:
+        size = n * P * 8
+        wire = 2 * (G - 1) / G * size
+        what = f"ncclAllReduce(delta, {n}x{P} f64, sum)"
+    else:
+        S = -(-m_total // G)
+        size = G * (2 * n * S * 4 + S * 8)
+        wire = (G - 1) / G * size
+        what = "ncclAllGather(succ, pred int32 [G][n][S]; 1/C_k f64)"
+    return {"collective": what, "bytes_per_gpu": int(wire),
+            "modelled_ms": round(wire / 700e9 * 1e3, 4),
+            "model": "bytes_per_gpu / 700 GB/s NVLink-5 bus bandwidth (not measured: 1-GPU box)"}
+
+
+WORKLOADS = [
+    # name, n, m (0 = n), selection, deposits, G list, iterations, cpu iterations
+    ("d198", 198, 0, 0, (0, 1), (1,), 10, 10),
+    ("pr1002", 1002, 0, 0, (0, 1), (1,), 10, 2),
+    ("pr2392", 2392, 0, 0, (0, 1), (1, 2, 4, 8), 10, 2),
+    ("pr2392x8ants", 2392, 8 * 2392, 0, (0, 1), (1, 2, 4, 8), 5, 1),
+    ("synth10k_nn30", 10000, 0, 1, (0,), (1, 8), 3, 1),
+]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "workloads.json"))
+    ap.add_argument("--quick", action="store_true", help="fewer iterations, no CPU baseline")
+    ap.add_argument("--only", default="")
+    ap.add_argument("--no-cpu", action="store_true")
+    a = ap.parse_args()
+    import torch
+
+    from paper_1101_2678_b200 import aco
+
+    peaks = l2_and_hbm_peaks()
+    report = {"peaks": peaks, "gpu": torch.cuda.get_device_name(0), "workloads": []}
+    for name, n, m, sel, deps, Gs, iters, cpu_iters in WORKLOADS:
+        if a.only and name not in a.only.split(","):
+            continue
+        m_total = m or n
+        prob = aco.build_problem(aco.synthetic_instance(n))
+        for dep in deps:
+            for G in Gs:
+                it = 2 if a.quick else iters
+                t0 = time.time()
+                res = time_engine(aco, torch, prob, n, m, sel, dep, G, it, 2)
+                res["wall_s"] = round(time.time() - t0, 1)
+                entry = {"workload": name, "n": n, "m": m_total, "G": G,
+                         "selection": aco.selection_name(aco.Selection(sel)),
+                         "deposit": aco.deposit_name(aco.Deposit(dep)), **res,
+                         "roofline": rooflines(res, n, m_total, sel, dep, 30, peaks),
+                         "exchange": exchange_model(n, m_total, G, dep)}
+                if G > 1:
+                    entry["ants_per_s_job"] = round(m_total / (res["ms_per_iter"] * 1e-3), 1)
+                print(json.dumps(entry), flush=True)
+                report["workloads"].append(entry)
+        if not (a.quick or a.no_cpu):
+            # reference CPU: accumulate always; the O(n^4) gather family only at d198
+            for dep in deps:
+                if dep == 1 and n > 198:
+                    continue
+                t0 = time.time()
+                ref = cpu_reference(n, m, sel, dep, cpu_iters)
+                ref["wall_s"] = round(time.time() - t0, 1)
+                entry = {"workload": name, "n": n, "m": m_total, "impl": "reference-cpu",
+                         "deposit": aco.deposit_name(aco.Deposit(dep)), **ref}
+                print(json.dumps(entry), flush=True)
+                report["workloads"].append(entry)
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    with open(a.out, "w") as f:
+        json.dump(report, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
