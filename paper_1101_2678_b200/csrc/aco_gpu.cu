@@ -21,6 +21,7 @@
 #include "../../include/aco_gpu.h"
 #include "construct.cuh"
 #include "construct_pair.cuh"
+#include "construct_team.cuh"
 #include "host_model.hpp"
 #include "update.cuh"
 
@@ -90,6 +91,7 @@ struct aco_gpu_ctx {
     int rank = 0, world = 1, ant_begin = 0, ant_end = 0, mloc = 0, S = 0;
     int P64 = 0, PW = 0, NV = 0, V = 4, C = 0, R = 1, MAXR = 1, tabu_words = 0;
     int LA = 32;          // lanes sharing a streamed row (16: two ants per warp)
+    int team = 1;         // warps per ant (k_construct_team when > 1)
     int half_smem = 0;    // pair kernel: bytes per half
     double tau0 = 0.0;
     int64_t max_d = 0;
@@ -200,8 +202,63 @@ ConstructFn pick_roulette(int NV, int MAXR) {
     return k_construct_roulette<WT, 20, 8>;
 }
 
+template <int K>
+ConstructFn pick_team_k(int NV) {
+    switch (NV) {
+    case 2: return k_construct_team<K, 2>;
+    case 3: return k_construct_team<K, 3>;
+    case 4: return k_construct_team<K, 4>;
+    case 5: return k_construct_team<K, 5>;
+    case 6: return k_construct_team<K, 6>;
+    case 8: return k_construct_team<K, 8>;
+    case 10: return k_construct_team<K, 10>;
+    case 12: return k_construct_team<K, 12>;
+    case 16: return k_construct_team<K, 16>;
+    default: return k_construct_team<K, 20>;
+    }
+}
+ConstructFn pick_team(int K, int NV) {
+    if (K == 2) return pick_team_k<2>(NV);
+    if (K == 4) return pick_team_k<4>(NV);
+    return pick_team_k<8>(NV);
+}
+
+// Warps per ant for the fp32 roulette.  k_construct_team (K = 2/4/8 warps
+// per ant) is bit-exact but measured SLOWER than one warp per ant at every
+// colony size tried, including the latency-bound ones (pr2392, 299 ants:
+// 2.19 ms one warp/ant vs 2.46 / 2.53 / 2.79 ms for K = 2/4/8; pr1002,
+// m = n: 0.82 vs 1.02 ms; profiles/team_sweep_r01.txt): the per-step chain
+// is dominated by the row's L2 round trip and the walk/certification, which
+// a team does not shorten, plus the team's barrier.  So it is opt-in:
+// ACO_TEAM=K (K in {2,4,8}).
+constexpr int kTeamNV[] = {2, 3, 4, 5, 6, 8, 10, 12, 16, 20};
+int choose_team(const aco_gpu_ctx* c) {
+    if (c->cfg.selection != ACO_SEL_ROULETTE || c->stream_kind != ACO_STREAM_FP32) return 1;
+    int K = 1;
+    if (const char* e = std::getenv("ACO_TEAM")) K = std::atoi(e);
+    if (K != 2 && K != 4 && K != 8) return 1;
+    while (K > 1 && K * 32 * 4 * 20 < c->n) K /= 2; // must cover n in K rounds
+    return K;
+}
+
 void choose_stream_layout(aco_gpu_ctx* c) {
     c->V = (c->stream_kind == ACO_STREAM_FP64) ? 2 : 4;
+    c->team = choose_team(c);
+    if (c->team > 1) {
+        c->LA = 32;
+        c->NV = 20;
+        for (int nv : kTeamNV)
+            if (c->team * 32 * 4 * nv >= c->n) {
+                c->NV = nv;
+                break;
+            }
+        c->C = 4 * c->NV;
+        c->R = c->team;
+        c->MAXR = c->team;
+        c->PW = c->R * kLP * c->C;
+        c->tabu_words = c->R * c->C + 4;
+        return;
+    }
     // Two-ants-per-warp kernel (construct_pair.cuh): bit-exact, but measured
     // slower at pr2392 (4.98 vs 4.18 ms: 9 warps/SM cannot hide its ~3000-cycle
     // step), so it is opt-in for experiments.
@@ -356,6 +413,23 @@ void launch_construct(aco_gpu_ctx* c) {
             std::fprintf(stderr, "construct: %s\n", c->construct_desc.c_str());
         fn<<<grid, 32, smem, c->stream>>>(p);
         check_launch(c, "k_construct_roulette_pair");
+    } else if (c->cfg.selection == ACO_SEL_ROULETTE && c->team > 1) {
+        ConstructFn fn = pick_team(c->team, c->NV);
+        const size_t smem = 256 + static_cast<size_t>(c->PW) * 4 + smem1 +
+                            static_cast<size_t>((c->n + 31) / 32) * sizeof(double);
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * c->team, smem));
+        const int grid = std::max(1, std::min(c->mloc, per_sm * c->num_sms));
+        c->construct_grid = grid;
+        c->construct_desc = "k_construct_team<" + std::to_string(c->team) + "," +
+                            std::to_string(c->NV) + "> grid=" + std::to_string(grid) +
+                            " per_sm=" + std::to_string(per_sm) + " smem=" + std::to_string(smem) +
+                            " row=" + std::to_string(c->PW);
+        if (std::getenv("ACO_DEBUG"))
+            std::fprintf(stderr, "construct: %s\n", c->construct_desc.c_str());
+        fn<<<grid, 32 * c->team, smem, c->stream>>>(p);
+        check_launch(c, "k_construct_team");
     } else if (c->cfg.selection == ACO_SEL_ROULETTE) {
         ConstructFn fn = c->stream_kind == ACO_STREAM_FP64 ? pick_roulette<double>(c->NV, c->MAXR)
                                                            : pick_roulette<float>(c->NV, c->MAXR);
