@@ -116,6 +116,8 @@ struct aco_gpu_ctx {
     int32_t* d_scale = nullptr;
     int32_t* d_nn = nullptr;
     double* d_choice_nn = nullptr; // n x nn
+    int32_t* d_topk = nullptr;     // n x kTopK argmax cache (nn selection)
+    long long last_fb[2] = {0, 0}; // last construction: exact/full-scan, argmax fallbacks
     int32_t* d_tours = nullptr;
     int64_t* d_len = nullptr;
     double* d_inv = nullptr;   // [world][S]
@@ -309,6 +311,19 @@ void choose_stream_layout(aco_gpu_ctx* c) {
     c->tabu_words = c->R * c->C + 4;  // covers R*32*C cities; even, keeps the fp64 area 8-aligned
 }
 
+// nn selection: rebuild the per-row argmax cache after every choice update
+void launch_topk(aco_gpu_ctx* c) {
+    if (!c->d_topk) return;
+    const size_t smem = (static_cast<size_t>(c->P64) + 512 + kTopCap) * sizeof(double) +
+                        kTopCap * sizeof(int);
+    CK(cudaFuncSetAttribute(k_row_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_row_topk, 256, smem));
+    const int grid = std::max(1, std::min(c->n, std::max(1, per_sm) * c->num_sms));
+    k_row_topk<<<grid, 256, smem, c->stream>>>(c->d_choice, c->n, c->P64, c->d_topk);
+    check_launch(c, "k_row_topk");
+}
+
 void launch_rows(aco_gpu_ctx* c, int mode) {
     RowParams rp{};
     rp.tau = c->d_tau;
@@ -345,18 +360,24 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
         const int grid = std::max(1, std::min(c->n, per_sm * c->num_sms));
         k_rows_gather_warp<<<grid, 32, wsmem, c->stream>>>(rp);
         check_launch(c, "k_rows_gather_warp");
+        launch_topk(c);
         return;
     }
+    // the CTA kernel needs the shared row only for the gather fold and the
+    // permuted streamed copies (k_rows)
+    const bool use_row = mode == MODE_GATHER || rp.choice32 || rp.choice_perm64;
+    const size_t rsmem = use_row ? smem : 0;
     const int grid = std::min(c->n, c->num_sms * 8);
     if (smem > 48 * 1024) {
         CK(cudaFuncSetAttribute(k_rows<MODE_CHOICE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute(k_rows<MODE_GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute(k_rows<MODE_DELTA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
-    if (mode == MODE_CHOICE) k_rows<MODE_CHOICE><<<grid, 256, smem, c->stream>>>(rp);
-    else if (mode == MODE_GATHER) k_rows<MODE_GATHER><<<grid, 256, smem, c->stream>>>(rp);
-    else k_rows<MODE_DELTA><<<grid, 256, smem, c->stream>>>(rp);
+    if (mode == MODE_CHOICE) k_rows<MODE_CHOICE><<<grid, 256, rsmem, c->stream>>>(rp);
+    else if (mode == MODE_GATHER) k_rows<MODE_GATHER><<<grid, 256, rsmem, c->stream>>>(rp);
+    else k_rows<MODE_DELTA><<<grid, 256, rsmem, c->stream>>>(rp);
     check_launch(c, "k_rows");
+    launch_topk(c);
 }
 
 ConstructParams make_cp(aco_gpu_ctx* c) {
@@ -383,6 +404,8 @@ ConstructParams make_cp(aco_gpu_ctx* c) {
     p.seed = c->seed;
     p.timing = c->d_timing;
     p.half_smem = c->half_smem;
+    p.topk = c->d_topk;
+    p.topk_k = kTopK;
     return p;
 }
 
@@ -786,6 +809,9 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
             CK(cudaMemcpy(c->d_nn, nn_host.data(), nn_host.size() * sizeof(int32_t),
                           cudaMemcpyHostToDevice));
             CK(cudaMalloc(&c->d_choice_nn, nn_host.size() * sizeof(double)));
+            const char* tke = std::getenv("ACO_NN_TOPK"); // "0" disables the argmax cache
+            if (!(tke && tke[0] == '0'))
+                CK(cudaMalloc(&c->d_topk, static_cast<size_t>(n) * kTopK * sizeof(int32_t)));
         }
         const size_t ml = std::max(1, c->mloc);
         CK(cudaMalloc(&c->d_tours, ml * (n + 1) * sizeof(int32_t)));
@@ -863,7 +889,7 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
 #endif
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
-    void* bufs[] = {c->d_choice_nn, c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
+    void* bufs[] = {c->d_choice_nn, c->d_topk, c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
                     c->d_choice_p64, c->d_scale, c->d_nn, c->d_tours, c->d_len, c->d_inv,
                     c->d_succ, c->d_pred, c->d_delta, c->d_stats, c->d_best, c->d_fb};
     for (void* b : bufs)
@@ -881,7 +907,10 @@ int64_t aco_gpu_launch_count(const aco_gpu_ctx* c) { return c ? c->launches : 0;
 
 int32_t aco_gpu_describe(const aco_gpu_ctx* c, char* buf, int32_t len) {
     if (!c) return 0;
-    const std::string& d = c->construct_desc;
+    std::string d = c->construct_desc;
+    if (c->cfg.selection == ACO_SEL_NN)
+        d += " argmax_fallbacks=" + std::to_string(c->last_fb[1]) + " full_row_scans=" +
+             std::to_string(c->last_fb[0]) + (c->d_topk ? " topk=" + std::to_string(kTopK) : " topk=off");
     if (buf && len > 0) {
         const size_t k = std::min(d.size(), static_cast<size_t>(len - 1));
         std::memcpy(buf, d.data(), k);
@@ -932,6 +961,8 @@ aco_status aco_gpu_construct(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
         aco_gpu_iter_record tmp{};
         aco_gpu_iter_record* r = rec ? rec : &tmp;
         const long long fb0 = c->h_stats[6], fb1 = c->h_stats[7];
+        c->last_fb[0] = fb0;
+        c->last_fb[1] = fb1;
         fill_common(c, r);
         finish_stats(c, r);
         r->construct_ms = ev_ms(c, 0, 2);
@@ -986,6 +1017,8 @@ aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* to
         r->exchange_ms = ev_ms(c, 2, 3);
         r->choice_ms = (!gather_mode(c) && c->world == 1) ? ev_ms(c, 4, 5) : 0.0;
         r->fallbacks = c->h_stats[6] + c->h_stats[7];
+        c->last_fb[0] = c->h_stats[6];
+        c->last_fb[1] = c->h_stats[7];
         r->best_so_far = c->best_so_far;
         ++c->iteration;
     });

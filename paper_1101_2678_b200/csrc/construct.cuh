@@ -112,6 +112,8 @@ struct ConstructParams {
     uint64_t seed;
     unsigned long long* timing; // ACO_TIMING: [8] phase cycle totals
     int half_smem;              // two-ants-per-warp kernel: bytes of one half's shared area
+    const int32_t* topk;        // nn selection: n x topk_k argmax cache (k_row_topk) or null
+    int topk_k;
 };
 
 __device__ __forceinline__ bool tabu_test(const uint32_t* tabu, int j) {
@@ -179,10 +181,18 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // >= 256) in pieces with TMA, and every lane folds every weight from
 // broadcast shared loads (same address in all lanes), so the only dependence
 // chain is the reference's own sequential fp64 add.
+// Number of staging pieces (mbarrier phases) one exact_walk consumes; the
+// caller advances its phase by this parity (phase is passed by value so it
+// stays in a register in the hot loop).
+__host__ __device__ __forceinline__ int exact_walk_pieces(int n, uint32_t stage_bytes) {
+    const int piece = static_cast<int>(stage_bytes / 256) * 32;
+    return (n + piece - 1) / piece;
+}
+
 __device__ __noinline__ int exact_walk(const double* __restrict__ row, const uint32_t* tabu,
                                        int n, int words, double u, int lane,
                                        double* chunk_start, double* stage, uint32_t stage_bytes,
-                                       uint64_t* bar, uint32_t& phase) {
+                                       uint64_t* bar, uint32_t phase) {
     const int nch = (n + 31) >> 5;
     const int piece = static_cast<int>(stage_bytes / 256) * 32; // cities per piece (chunk-aligned)
     double acc = 0.0;
@@ -818,6 +828,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                 next = exact_walk(p.w64 + static_cast<size_t>(cur) * p.P64, tabu, n,
                                   p.tabu_words, u, lane, chunk_start,
                                   reinterpret_cast<double*>(buf), row_bytes & ~255u, bar, phase);
+                phase ^= static_cast<uint32_t>(exact_walk_pieces(n, row_bytes & ~255u) & 1);
                 ++fb;
             }
             TICK(4);
@@ -873,7 +884,7 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
         }
         __syncwarp();
         int cur = start;
-        unsigned long long fb = 0;
+        unsigned long long fb = 0, fb_full = 0;
         double ubatch = 0.0;
         for (int step = 1; step < n; ++step) {
             const double* __restrict__ row = p.w64 + static_cast<size_t>(cur) * p.P64;
@@ -898,9 +909,11 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
                     double w = 0.0;
                     bool un = false;
                     if (q < nn) {
+                        // id and weight issued together: one L2 round trip per step
                         j = nb[q];
+                        const double wq0 = wn[q];
                         un = !tabu_test(tabu, j);
-                        if (un) w = wn[q];
+                        w = un ? wq0 : 0.0;
                     }
                     jm[k] = j;
                     const unsigned unb = __ballot_sync(kFull, un);
@@ -934,7 +947,35 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
                     if (next < 0) next = last_pos >= 0 ? last_pos : first_un; // :103-105
                 }
             } else {
-                // argmax over all unvisited, lowest index on ties (:108-120)
+                // argmax over all unvisited, lowest index on ties (:108-120):
+                // first the row's top-K cache (k_row_topk): its first
+                // unvisited entry IS the argmax; a full scan only when every
+                // cached entry is visited (or the row's cache is invalid).
+                ++fb;
+                if (p.topk) {
+                    const int32_t* tk = p.topk + static_cast<size_t>(cur) * p.topk_k;
+                    int ids[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) ids[r] = 32 * r < p.topk_k ? tk[32 * r + lane] : -1;
+                    if (__shfl_sync(kFull, ids[0], 0) != -2) {
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const bool un = ids[r] >= 0 && !tabu_test(tabu, ids[r]);
+                            const unsigned b = __ballot_sync(kFull, un);
+                            if (b && next < 0) next = __shfl_sync(kFull, ids[r], __ffs(b) - 1);
+                        }
+                    }
+                    if (next >= 0) {
+                        if (lane == 0) {
+                            tabu[next >> 5] |= 1u << (next & 31);
+                            tour[step] = next;
+                        }
+                        __syncwarp();
+                        cur = next;
+                        continue;
+                    }
+                }
+                ++fb_full;
                 double bw = -1.0;
                 int bj = -1;
                 const double2* r2 = reinterpret_cast<const double2*>(row);
@@ -984,7 +1025,6 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
                     if (oj >= 0 && (bj < 0 || ow > bw || (ow == bw && oj < bj))) { bw = ow; bj = oj; }
                 }
                 next = bj;
-                ++fb;
             }
             if (lane == 0) {
                 tabu[next >> 5] |= 1u << (next & 31);
@@ -996,6 +1036,7 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
         if (lane == 0) {
             tour[n] = start;
             if (fb) atomicAdd(p.argmax_fallbacks, fb);
+            if (fb_full) atomicAdd(p.fallbacks, fb_full);
         }
         __syncwarp();
     }

@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(32 * K) k_construct_team(ConstructParams p) {
                                       p.tabu_words, u, lane, chunk_start,
                                       reinterpret_cast<double*>(buf), row_bytes & ~255u,
                                       bar_fb + warp, phase_fb);
+                    phase_fb ^= static_cast<uint32_t>(exact_walk_pieces(n, row_bytes & ~255u) & 1);
                     ++fb;
                 }
                 __syncwarp();

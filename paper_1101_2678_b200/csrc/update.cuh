@@ -208,16 +208,29 @@ __device__ __forceinline__ double tau_pow(double t, double alpha) {
     return pow(t, alpha);         // parity unpinned for other alpha
 }
 
+// One CTA (256 threads) per row.  The elementwise pass works on column PAIRS
+// (16-byte tau / choice / delta accesses, 8-byte dist) in batches of EB pairs
+// per thread, all loads of a batch issued before any eta^beta gather and all
+// gathers before the arithmetic, so each thread keeps 3*EB independent memory
+// requests in flight.  Pad columns (n <= j < P64) compute 0 (tau pad = 0) and
+// are written like the others.  The shared row (P64 doubles) is used only
+// when something needs the finished row: the gather fold, the permuted
+// streamed copies (row max first) and the nn weights; otherwise the kernel
+// runs with no dynamic shared memory and full occupancy.
 template <int MODE>
-__global__ void __launch_bounds__(256) k_rows(RowParams p) {
-    extern __shared__ double rowbuf[]; // P64 doubles
+__global__ void __launch_bounds__(256, 3) k_rows(RowParams p) {
+    extern __shared__ double rowbuf[]; // P64 doubles when use_row
     __shared__ double s_max[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = p.n;
+    const bool use_row = MODE == MODE_GATHER || p.choice32 || p.choice_perm64;
+    const bool need_sync = use_row || p.choice_nn;
+    const int n2 = p.P64 >> 1;
+    constexpr int EB = MODE == MODE_CHOICE ? 4 : 3;
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
         double* trow = p.tau + static_cast<size_t>(i) * p.P64;
         if constexpr (MODE == MODE_GATHER) {
-            for (int j = tid; j < n; j += blockDim.x) rowbuf[j] = 0.0;
+            for (int j = tid; j < p.P64; j += blockDim.x) rowbuf[j] = 0.0;
             __syncthreads();
             // Contributions to column c arrive in ascending global ant order
             // (shards are contiguous ant ranges); warp `warp` owns columns
@@ -252,34 +265,69 @@ __global__ void __launch_bounds__(256) k_rows(RowParams p) {
             __syncthreads();
         }
         double mx = 0.0;
-        const int32_t* drow = p.dist + static_cast<size_t>(i) * p.P64;
-        for (int j = tid; j < n; j += blockDim.x) {
-            double t = trow[j];
-            if constexpr (MODE == MODE_GATHER) {
-                t = __dadd_rn(__dmul_rn(t, p.keep), rowbuf[j]);
-                trow[j] = t;
-            } else if constexpr (MODE == MODE_DELTA) {
-                double* drw = p.delta + static_cast<size_t>(i) * p.P64;
-                t = __dadd_rn(__dmul_rn(t, p.keep), drw[j]);
-                drw[j] = 0.0;
-                trow[j] = t;
+        const int2* drow2 = reinterpret_cast<const int2*>(p.dist + static_cast<size_t>(i) * p.P64);
+        const double2* erow2 =
+            p.etab ? reinterpret_cast<const double2*>(p.etab + static_cast<size_t>(i) * p.P64) : nullptr;
+        double2* trow2 = reinterpret_cast<double2*>(trow);
+        double2* crow2 = reinterpret_cast<double2*>(p.choice64 + static_cast<size_t>(i) * p.P64);
+        double2* drw2 = MODE == MODE_DELTA
+                            ? reinterpret_cast<double2*>(p.delta + static_cast<size_t>(i) * p.P64)
+                            : nullptr;
+        for (int b0 = tid; b0 < n2; b0 += 256 * EB) {
+            double2 tv[EB], dl[EB], eb[EB];
+            int2 dv[EB];
+#pragma unroll
+            for (int u = 0; u < EB; ++u) {
+                const int j2 = b0 + 256 * u;
+                const bool in = j2 < n2;
+                tv[u] = in ? trow2[j2] : make_double2(0.0, 0.0);
+                dv[u] = (in && !erow2) ? __ldg(drow2 + j2) : make_int2(0, 0);
+                if constexpr (MODE == MODE_DELTA) dl[u] = in ? drw2[j2] : make_double2(0.0, 0.0);
+                if constexpr (MODE == MODE_GATHER) {
+                    dl[u] = in ? reinterpret_cast<const double2*>(rowbuf)[j2] : make_double2(0.0, 0.0);
+                }
             }
-            const double eb = p.etab ? p.etab[static_cast<size_t>(i) * p.P64 + j] : p.lut[drow[j]];
-            const double c = (j == i) ? 0.0 : __dmul_rn(tau_pow(t, p.alpha), eb);
-            p.choice64[static_cast<size_t>(i) * p.P64 + j] = c;
-            rowbuf[j] = c;
-            mx = fmax(mx, c);
+#pragma unroll
+            for (int u = 0; u < EB; ++u) {
+                const int j2 = b0 + 256 * u;
+                if (j2 < n2) {
+                    eb[u] = erow2 ? __ldg(erow2 + j2)
+                                  : make_double2(__ldg(p.lut + dv[u].x), __ldg(p.lut + dv[u].y));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < EB; ++u) {
+                const int j2 = b0 + 256 * u;
+                if (j2 < n2) {
+                    const int j = 2 * j2;
+                    double2 t = tv[u];
+                    if constexpr (MODE == MODE_GATHER || MODE == MODE_DELTA) {
+                        // pheromone.hpp:183 (evaporate) then :220 / the summed delta
+                        t.x = __dadd_rn(__dmul_rn(t.x, p.keep), dl[u].x);
+                        t.y = __dadd_rn(__dmul_rn(t.y, p.keep), dl[u].y);
+                        trow2[j2] = t;
+                        if constexpr (MODE == MODE_DELTA) drw2[j2] = make_double2(0.0, 0.0);
+                    }
+                    double2 c;
+                    c.x = (j == i) ? 0.0 : __dmul_rn(tau_pow(t.x, p.alpha), eb[u].x);
+                    c.y = (j + 1 == i) ? 0.0 : __dmul_rn(tau_pow(t.y, p.alpha), eb[u].y);
+                    crow2[j2] = c;
+                    if (use_row) reinterpret_cast<double2*>(rowbuf)[j2] = c;
+                    mx = fmax(mx, fmax(c.x, c.y));
+                }
+            }
         }
         if (p.choice32 || p.choice_perm64) {
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, off));
             if (lane == 0) s_max[warp] = mx;
         }
-        __syncthreads();
+        if (need_sync) __syncthreads(); // also orders this block's choice64 stores
         if (p.choice_nn) { // the nn list's weights, contiguous per row (L2-resident)
+            const double* src = use_row ? rowbuf : p.choice64 + static_cast<size_t>(i) * p.P64;
             for (int q = tid; q < p.nn; q += blockDim.x)
                 p.choice_nn[static_cast<size_t>(i) * p.nn + q] =
-                    rowbuf[p.nn_lists[static_cast<size_t>(i) * p.nn + q]];
+                    src[p.nn_lists[static_cast<size_t>(i) * p.nn + q]];
         }
         if (p.choice32) {
             double rmx = 0.0;
@@ -294,7 +342,7 @@ __global__ void __launch_bounds__(256) k_rows(RowParams p) {
             write_stream_row<2>(p.choice_perm64 + static_cast<size_t>(i) * p.PW, rowbuf, n, p.PW,
                                 p.C, p.LA, 0, tid, blockDim.x);
         }
-        __syncthreads();
+        if (need_sync) __syncthreads();
     }
 }
 
@@ -419,6 +467,93 @@ __global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
 }
 
 // Device Philox self-test (aco_gpu_philox_uniform).
+// ---------------------------------------------------------------------------
+// Top-KT cache of every choice row for the nn selection's argmax fallback
+// (select_next_nn, construction.hpp:108-120: argmax of w over the unvisited
+// cities, the lowest index on ties).  Row i's list holds the KT best cities
+// under the total order (w desc, index asc).  For any tabu set, the FIRST
+// unvisited entry of the list is that argmax: every unvisited city outside
+// the list is after every list entry in the order.  Only when all KT entries
+// are visited does the construction scan the whole row.  A row whose
+// candidate set overflows the scratch is marked invalid (entry 0 = -2) and
+// always scans.  Rebuilt after every choice_info recomputation.
+//
+// Per row (one 256-thread CTA): the row is staged in shared memory; 512
+// strided sub-range maxima; M = the KT-th largest of them (by rank), so at
+// least KT cities have w >= M; those cities are collected and ranked by the
+// total order.  Bytes: 8 n^2 read + 4 KT n written.
+constexpr int kTopK = 128;
+constexpr int kTopCap = 768;
+
+__global__ void __launch_bounds__(256) k_row_topk(const double* __restrict__ choice, int n, int P64,
+                                                  int32_t* __restrict__ topk) {
+    extern __shared__ double tk_smem[];
+    double* row = tk_smem;                 // P64
+    double* smax = row + P64;              // 512
+    double* cv = smax + 512;               // kTopCap
+    int* ci = reinterpret_cast<int*>(cv + kTopCap); // kTopCap
+    __shared__ int s_cnt;
+    __shared__ double s_min[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        const double* src = choice + static_cast<size_t>(i) * P64;
+        for (int j = tid; j < n; j += 256) row[j] = src[j];
+        if (tid == 0) s_cnt = 0;
+        __syncthreads();
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const int q = tid + 256 * s;
+            double mx = -1.0;
+            for (int j = q; j < n; j += 512) mx = fmax(mx, row[j]);
+            smax[q] = mx;
+        }
+        __syncthreads();
+        double mine = 1e308;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const double v = smax[tid + 256 * s];
+            int r = 0;
+            for (int q = 0; q < 512; ++q) r += smax[q] > v ? 1 : 0;
+            if (r < kTopK && v >= 0.0) mine = fmin(mine, v);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mine = fmin(mine, __shfl_xor_sync(kFull, mine, off));
+        if (lane == 0) s_min[warp] = mine;
+        __syncthreads();
+        double M = s_min[0];
+        for (int w = 1; w < 8; ++w) M = fmin(M, s_min[w]);
+        for (int j = tid; j < n; j += 256) {
+            const double v = row[j];
+            if (v >= M) {
+                const int pos = atomicAdd(&s_cnt, 1);
+                if (pos < kTopCap) {
+                    cv[pos] = v;
+                    ci[pos] = j;
+                }
+            }
+        }
+        __syncthreads();
+        const int c = s_cnt;
+        int32_t* out = topk + static_cast<size_t>(i) * kTopK;
+        if (c > kTopCap) {
+            if (tid == 0) out[0] = -2; // invalid: the construction scans the row
+        } else {
+            for (int a = tid; a < c; a += 256) {
+                const double va = cv[a];
+                const int ja = ci[a];
+                int r = 0;
+                for (int b = 0; b < c; ++b) {
+                    const double vb = cv[b];
+                    r += (vb > va || (vb == va && ci[b] < ja)) ? 1 : 0;
+                }
+                if (r < kTopK) out[r] = ja;
+            }
+            for (int r = c + tid; r < kTopK; r += 256) out[r] = -1; // n < KT: end of list
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void k_philox_test(uint64_t seed, uint32_t it, uint32_t ant, int count,
                               const uint32_t* steps, const uint32_t* draws, double* out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;

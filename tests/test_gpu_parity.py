@@ -251,3 +251,51 @@ def test_team_construction_pr2392_subset(aco, oracle, monkeypatch, K):
         t_ref, l_ref, _ = oracle.construct(prob.dist, oracle.choice(prob.dist, tau), 1, 0, 700, 764)
         assert np.array_equal(t, t_ref)
         assert np.array_equal(l, l_ref)
+
+
+@pytest.mark.parametrize("topk", ["1", "0"])
+def test_nn_argmax_cache_bit_exact(aco, oracle, monkeypatch, topk):
+    """The nn selection's argmax fallback through the per-row top-K cache
+    (k_row_topk) and through the full-row scan (ACO_NN_TOPK=0) both give the
+    reference's tours; n=3000 with nn=8 makes the fallback frequent, and the
+    cache must take most of them."""
+    monkeypatch.setenv("ACO_NN_TOPK", topk)
+    n, nn = 3000, 8
+    prob, eng = make(aco, n, selection=1, deposit=1, nn=nn, ant_range=(0, 96))
+    with eng:
+        nnl = oracle.nn_lists(prob.dist, nn)
+        tau = np.full((n, n), eng.tau0)
+        ch = oracle.choice(prob.dist, tau)
+        eng.construct()
+        desc = eng.describe()
+        t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, 0, 0, 96, selection=1, nn_lists=nnl)
+        t, l = eng.ants()
+        assert np.array_equal(t, t_ref)
+        assert np.array_equal(l, l_ref)
+        fields = dict(kv.split("=") for kv in desc.split() if "=" in kv)
+        argmax, full = int(fields["argmax_fallbacks"]), int(fields["full_row_scans"])
+        assert argmax > 1000
+        if topk == "1":
+            assert fields["topk"] == "128" and full < argmax // 2
+        else:
+            assert fields["topk"] == "off" and full == argmax
+
+
+def test_gather_cta_row_kernel_bit_exact(aco, oracle):
+    """n = 4500: a row of doubles no longer fits one warp's shared slice, so
+    the gather update runs the CTA-per-row k_rows<GATHER> (paired, batched
+    epilogue) — bit-exact tau and choice over two iterations."""
+    n, m = 4500, 64
+    prob, eng = make(aco, n, deposit=1, m=m)
+    with eng:
+        tau = np.full((n, n), eng.tau0)
+        for it in range(2):
+            ch = oracle.choice(prob.dist, tau)
+            assert np.array_equal(eng.choice(), ch)
+            eng.run_iteration()
+            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, 0, m)
+            t, l = eng.ants()
+            assert np.array_equal(t, t_ref), f"iteration {it}"
+            tau = oracle.update(tau, t_ref, l_ref, 0.5, 1)
+            assert np.array_equal(eng.pheromone(), tau)
+        assert np.array_equal(eng.choice(), oracle.choice(prob.dist, tau))
