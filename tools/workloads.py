@@ -18,9 +18,13 @@ Rooflines:
   construction (nn):       m_local*(n-1)*(nn*(8+4)) list bytes + one fp64 row
       (n*8) per argmax-fallback step, over the same L2 peak (the lists are
       L2-resident; the fallback rows stream from HBM at 10k);
-  update (accumulate):     evaporate 16*n*P + deposit 2*m*n red.f64 (8 B each)
-      + tours 4*m*(n+1) + choice epilogue (8+4+8+4)*n*P, over HBM peak;
-  update (gather):         (8+8+4+8+4)*n*P + 16*m*n + 8*m, over HBM peak.
+  update (accumulate, G=1): evaporate 16*n*P + deposit 2*m*n red.f64 (8 B each)
+      + tours 4*m*(n+1) + choice epilogue (8+4+8+S)*n*P, over HBM peak;
+  update (accumulate, G>1): k_rows<DELTA> (8+8+8+8+4+8+S)*n*P (the local
+      red.f64 deposit runs in the construction phase);
+  update (gather):         (8+8+4+8+S)*n*P + 16*m*n + 8*m, over HBM peak;
+  S = 4 for the roulette's fp32 stream, 0 for nn; nn adds the top-K rebuild's
+      8*n*P re-read of the choice rows.
 """
 from __future__ import annotations
 
@@ -104,10 +108,14 @@ def rooflines(res, n, m_total, selection, deposit, nn, peaks):
         b_c = ml * (n - 1) * nn * (8 + 4) + res["fallback_steps_per_iter"] * n * 8
     else:
         b_c = ml * (n - 1) * n * 4
-    if deposit == 0:
-        b_u = 16 * n * P + 2 * m_total * n * 8 + 4 * m_total * (n + 1) + 24 * n * P
-    else:
-        b_u = 32 * n * P + 16 * m_total * n + 8 * m_total
+    s32 = 4 if selection == 0 else 0          # the fp32 streamed copy (roulette only)
+    topk = 8 * n * P if selection == 1 else 0  # k_row_topk re-reads the choice rows
+    if deposit == 0 and res.get("G", 1) > 1:   # k_rows<DELTA>: tau, delta r/w, dist, choice
+        b_u = (8 + 8 + 8 + 8 + 4 + 8 + s32) * n * P + topk
+    elif deposit == 0:                         # evaporate + red.f64 + k_rows<CHOICE>
+        b_u = 16 * n * P + 2 * m_total * n * 8 + 4 * m_total * (n + 1) + (8 + 4 + 8 + s32) * n * P + topk
+    else:                                      # k_rows gather: tau r/w, dist, choice + succ/pred
+        b_u = (8 + 8 + 4 + 8 + s32) * n * P + 16 * m_total * n + 8 * m_total + topk
     c_gbs = b_c / (res["construct_kernel_ms"] * 1e-3) / 1e9
     u_gbs = b_u / (res["update_ms"] * 1e-3) / 1e9
     return {
@@ -171,6 +179,7 @@ def main():
                 it = 2 if a.quick else iters
                 t0 = time.time()
                 res = time_engine(aco, torch, prob, n, m, sel, dep, G, it, 2)
+                res["G"] = G
                 res["wall_s"] = round(time.time() - t0, 1)
                 entry = {"workload": name, "n": n, "m": m_total, "G": G,
                          "selection": aco.selection_name(aco.Selection(sel)),
