@@ -7,7 +7,9 @@ synthetic pr2392-size EUC_2D instance of SURVEY.md App. B (splitmix64 seed
 42, integer coords in [0, 10000]), m = n = 2392 ants, alpha=1 beta=2 rho=0.5
 seed=1, full roulette construction.  Headline deposit: accumulate (atomic
 scatter, the reference CLI default); the deterministic scatter-to-gather
-deposit is timed beside it ("compare").  N > 1 (torchrun): the colony is
+deposit is timed beside it ("compare"), and BASELINE config 4 (8 x 2392
+ants sharded over the N GPUs) is reported as "sharded_8x_ants" with its
+ants/s.  N > 1 (torchrun): the colony is
 sharded by ants over the ranks (strong scaling: m = n fixed), NCCL exchange
 inside the engine, max-over-ranks device time.
 
@@ -233,8 +235,8 @@ def run_ours(args):
     prob = aco.build_problem(spec)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")
 
-    def make_engine(deposit):
-        cfg = aco.RunConfig(params=aco.Parameters(m=0, seed=1),
+    def make_engine(deposit, m=0):
+        cfg = aco.RunConfig(params=aco.Parameters(m=m, seed=1),
                             selection=aco.SelectionStrategy(aco.Selection.roulette_full),
                             deposit=aco.DepositStrategy(deposit), device=device,
                             rank=rank, world=world, nccl_id=nccl_id)
@@ -310,6 +312,18 @@ def run_ours(args):
     con_g = max_over_ranks(statistics.mean(r.construct_ms for r in recs_g))
     eng_g.close()
 
+    # ---- BASELINE config 4: 8 x 2392 ants sharded over the N ranks (the
+    # north star's "near-linear ants/sec" configuration), accumulate deposit
+    m8 = 8 * N_CITIES
+    eng_8, _ = make_engine(aco.Deposit.accumulate, m=m8)
+    st8 = max(3, min(args.steps, 10))
+    per_8, recs_8, _, _ = device_timed(eng_8, st8, args.warmup)
+    ms_8 = max_over_ranks(statistics.mean(per_8))
+    con_8 = max_over_ranks(statistics.mean(r.construct_ms for r in recs_8))
+    upd_8 = max_over_ranks(statistics.mean(r.update_ms for r in recs_8))
+    exch_8 = max_over_ranks(statistics.mean(r.exchange_ms for r in recs_8))
+    eng_8.close()
+
     if rank != 0:
         if dist_on:
             dist.barrier()
@@ -358,6 +372,13 @@ def run_ours(args):
                                        "update_ms": round(upd_g, 4),
                                        "tau": "bit-exact vs reference"},
                     "accumulate": {"tau": "atomic, <=1e-5 relative vs reference"}},
+        "sharded_8x_ants": {"workload": "BASELINE config 4: pr2392, m = 8*2392 = 19136 ants "
+                                        f"sharded over {world} GPU(s), accumulate",
+                            "m": m8, "ants_per_gpu": -(-m8 // world), "steps": st8,
+                            "ms_per_iter": round(ms_8, 4), "construct_ms": round(con_8, 4),
+                            "update_ms": round(upd_8, 4), "exchange_ms": round(exch_8, 4),
+                            "ants_per_s": round(m8 / (ms_8 * 1e-3), 1),
+                            "scaling": "strong over the fixed 19136-ant colony"},
         "roofline": {"bound": "l2", "kernel": kernel_desc,
                      "achieved": round(achieved, 1), "peak": l2_peak, "unit": "GB/s",
                      "frac": round(achieved / l2_peak, 4) if l2_peak else None,

@@ -299,3 +299,21 @@ def test_gather_cta_row_kernel_bit_exact(aco, oracle):
             tau = oracle.update(tau, t_ref, l_ref, 0.5, 1)
             assert np.array_equal(eng.pheromone(), tau)
         assert np.array_equal(eng.choice(), oracle.choice(prob.dist, tau))
+
+
+def test_gather_fold_converged_colony_bit_exact(aco, oracle):
+    """The warp-per-row gather fold reproduces the reference's
+    scatter-to-gather tau over iterations in which the colony concentrates on
+    few edges (rho = 0.9: many equal columns inside each 16-ant chunk)."""
+    n = 1002
+    prob, eng = make(aco, n, deposit=1, rho=0.9)
+    with eng:
+        tau = np.full((n, n), eng.tau0)
+        for it in range(3):
+            ch = oracle.choice(prob.dist, tau)
+            eng.run_iteration()
+            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, 0, n)
+            t, l = eng.ants()
+            assert np.array_equal(t, t_ref), f"iteration {it}"
+            tau = oracle.update(tau, t_ref, l_ref, 0.9, 1)
+            assert np.array_equal(eng.pheromone(), tau)
