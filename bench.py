@@ -225,11 +225,15 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", device))
-    nccl_id = None
-    if dist_on:
+
+    def fresh_nccl_id():
+        # one ncclUniqueId per communicator: an id's bootstrap root serves a
+        # single ncclCommInitRank, so every engine gets its own
+        if not dist_on:
+            return None
         obj = [aco.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        return obj[0]
 
     spec = aco.synthetic_instance(N_CITIES)
     prob = aco.build_problem(spec)
@@ -239,7 +243,7 @@ def run_ours(args):
         cfg = aco.RunConfig(params=aco.Parameters(m=m, seed=1),
                             selection=aco.SelectionStrategy(aco.Selection.roulette_full),
                             deposit=aco.DepositStrategy(deposit), device=device,
-                            rank=rank, world=world, nccl_id=nccl_id)
+                            rank=rank, world=world, nccl_id=fresh_nccl_id())
         t0 = time.time()
         eng = aco.Engine(prob, cfg)
         return eng, (time.time() - t0) * 1e3

@@ -105,6 +105,7 @@ struct aco_gpu_ctx {
 
     // device buffers
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr; // D2H of the tours, overlapped with the update
     cudaEvent_t ev[6] = {};
     int32_t* d_dist = nullptr;
     double* d_lut = nullptr;
@@ -764,6 +765,7 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         CK(cudaSetDevice(c->device));
         CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
         choose_stream_layout(c);
         c->P64 = round_up(n, 32);
@@ -888,6 +890,7 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
     }
 #endif
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
     void* bufs[] = {c->d_choice_nn, c->d_topk, c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
                     c->d_choice_p64, c->d_scale, c->d_nn, c->d_tours, c->d_len, c->d_inv,
@@ -898,6 +901,7 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     delete c;
 }
 
@@ -999,17 +1003,24 @@ aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* to
             CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
             finish_stats(c, r);
         }
+        // the tours are final once the construction phase (ev[2]) is done:
+        // copy them out on a second stream while the update runs (the update
+        // only reads them), and join before returning
+        if (tours_out || lengths_out) {
+            CK(cudaStreamWaitEvent(c->copy_stream, c->ev[2], 0));
+            if (tours_out)
+                CK(cudaMemcpyAsync(tours_out, c->d_tours, sizeof(int32_t) * c->mloc * (c->n + 1),
+                                   cudaMemcpyDeviceToHost, c->copy_stream));
+            if (lengths_out)
+                CK(cudaMemcpyAsync(lengths_out, c->d_len, sizeof(int64_t) * c->mloc,
+                                   cudaMemcpyDeviceToHost, c->copy_stream));
+        }
         do_update(c);
-        if (tours_out)
-            CK(cudaMemcpyAsync(tours_out, c->d_tours, sizeof(int32_t) * c->mloc * (c->n + 1),
-                               cudaMemcpyDeviceToHost, c->stream));
-        if (lengths_out)
-            CK(cudaMemcpyAsync(lengths_out, c->d_len, sizeof(int64_t) * c->mloc,
-                               cudaMemcpyDeviceToHost, c->stream));
         if (c->world == 1 || c->external)
             CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(c->h_stats + 6, c->d_fb, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
+        if (tours_out || lengths_out) CK(cudaStreamSynchronize(c->copy_stream));
         if (c->world == 1 || c->external) finish_stats(c, r);
         r->construct_ms = ev_ms(c, 0, 2);
         r->construct_kernel_ms = ev_ms(c, 0, 1);

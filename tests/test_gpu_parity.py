@@ -317,3 +317,43 @@ def test_gather_fold_converged_colony_bit_exact(aco, oracle):
             assert np.array_equal(t, t_ref), f"iteration {it}"
             tau = oracle.update(tau, t_ref, l_ref, 0.9, 1)
             assert np.array_equal(eng.pheromone(), tau)
+
+
+def _spec_dup(aco, n, seed=5):
+    """EUC_2D instance with duplicated and collinear cities (zero distances:
+    eta = 1 by model.hpp:142, many equal weights)."""
+    rng = np.random.default_rng(seed)
+    xs = rng.integers(0, 50, n).astype(np.float64)
+    ys = rng.integers(0, 50, n).astype(np.float64)
+    xs[n // 2:] = xs[: n - n // 2]  # every city of the second half duplicates one of the first
+    ys[n // 2:] = ys[: n - n // 2]
+    ys[: n // 4] = 7.0               # a collinear run
+    return aco.InstanceSpec(name=f"dup{n}", dimension=n, xs=xs, ys=ys)
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 33, 97])
+@pytest.mark.parametrize("selection", [0, 1, 2])
+@pytest.mark.parametrize("dup", [False, True])
+def test_small_and_degenerate_instances_bit_exact(aco, oracle, n, selection, dup):
+    """Edge cases: tiny n (one-lane chunks, a single unvisited city, n < warp
+    width), duplicate cities (zero distances) and ties, for every selection
+    rule; gather-path tau bit-exact over three iterations."""
+    if dup and n < 5:
+        pytest.skip("duplicates need n >= 5")
+    nn = min(30, n - 1)
+    spec = _spec_dup(aco, n) if dup else aco.synthetic_instance(n)
+    prob, eng = make(aco, n, selection=selection, deposit=1, nn=nn, spec=spec)
+    with eng:
+        nnl = oracle.nn_lists(prob.dist, nn) if selection == 1 else None
+        tau = np.full((n, n), eng.tau0)
+        for it in range(3):
+            ch = oracle.choice(prob.dist, tau)
+            assert np.array_equal(eng.choice(), ch)
+            eng.run_iteration()
+            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, 0, n, selection=selection,
+                                               nn_lists=nnl)
+            t, l = eng.ants()
+            assert np.array_equal(t, t_ref), f"iteration {it}"
+            assert np.array_equal(l, l_ref)
+            tau = oracle.update(tau, t_ref, l_ref, 0.5, 1)
+            assert np.array_equal(eng.pheromone(), tau)
