@@ -315,13 +315,10 @@ void choose_stream_layout(aco_gpu_ctx* c) {
 // nn selection: rebuild the per-row argmax cache after every choice update
 void launch_topk(aco_gpu_ctx* c) {
     if (!c->d_topk) return;
-    const size_t smem = (static_cast<size_t>(c->P64) + 512 + kTopCap) * sizeof(double) +
-                        kTopCap * sizeof(int);
-    CK(cudaFuncSetAttribute(k_row_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_row_topk, 256, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_row_topk, 256, 0));
     const int grid = std::max(1, std::min(c->n, std::max(1, per_sm) * c->num_sms));
-    k_row_topk<<<grid, 256, smem, c->stream>>>(c->d_choice, c->n, c->P64, c->d_topk);
+    k_row_topk<<<grid, 256, 0, c->stream>>>(c->d_choice, c->n, c->P64, c->d_topk);
     check_launch(c, "k_row_topk");
 }
 

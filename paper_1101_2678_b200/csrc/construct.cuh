@@ -895,7 +895,57 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
                                         static_cast<uint32_t>(step + lane), 0);
             const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
             int next = -1;
-            // fold: lane q of pass k holds member 32k+q
+            bool exhausted = false; // every list member visited: argmax fallback
+            if (nn <= 32) {
+                // Fast path: one fp64 warp scan instead of the sequential
+                // fold, then CERTIFY the crossing against the reference's
+                // sequential sums (as in k_construct_roulette): every scan
+                // prefix P_q and the reference's S_q are within e*X_q of the
+                // exact prefix X_q (e: 5 scan levels + nn sequential adds,
+                // all summands >= 0), and t_ref = fl(u*S_n) within Mt of
+                // t = u*T.  Uncertain steps (~never at e ~ 2^-47) take the
+                // exact fold below.
+                const int q = lane;
+                int j = -1;
+                double w = 0.0;
+                bool un = false;
+                if (q < nn) {
+                    j = nb[q];
+                    const double wq0 = wn[q];
+                    un = !tabu_test(tabu, j);
+                    w = un ? wq0 : 0.0;
+                }
+                const unsigned unb = __ballot_sync(kFull, un);
+                if (!unb) {
+                    exhausted = true;
+                } else {
+                    double P = w;
+#pragma unroll
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const double y = __shfl_up_sync(kFull, P, off);
+                        if (lane >= off) P += y;
+                    }
+                    const double T = __shfl_sync(kFull, P, 31);
+                    if (!(T > 0.0)) {
+                        next = __shfl_sync(kFull, j, __ffs(unb) - 1); // :89-92, exact
+                    } else {
+                        const double Eu = __shfl_up_sync(kFull, P, 1); // every lane shuffles
+                        const double E = lane == 0 ? 0.0 : Eu;
+                        const double t = u * T;
+                        const unsigned cr = __ballot_sync(kFull, q < nn && w > 0.0 && P > t);
+                        if (cr) {
+                            const int J = __ffs(cr) - 1;
+                            const double PJ = __shfl_sync(kFull, P, J);
+                            const double EJ = __shfl_sync(kFull, E, J);
+                            const double e = 48.0 * 0x1.0p-53;
+                            const double Mt = (e + 0x1.0p-51) * u * T * (1.0 + 0x1.0p-16) + 0x1.0p-1074;
+                            if (PJ * (1.0 - e) > t + Mt && EJ + e * T < t - Mt)
+                                next = __shfl_sync(kFull, j, J);
+                        }
+                    }
+                }
+            }
+            // exact sequential fold: lane q of pass k holds member 32k+q
             double acc = 0.0;
             int first_un = -1, last_pos = -1;
             double mine[2] = {0.0, 0.0};
@@ -903,7 +953,7 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 const int q0 = 32 * k;
-                if (q0 < nn) {
+                if (q0 < nn && next < 0 && !exhausted) {
                     const int q = q0 + lane;
                     int j = -1;
                     double w = 0.0;
@@ -931,7 +981,9 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
                     }
                 }
             }
-            if (first_un >= 0) {
+            if (next >= 0) {
+                // certified fast path (or its exact zero-total branch)
+            } else if (first_un >= 0) {
                 const double total = acc;
                 if (!(total > 0.0)) {
                     next = first_un;                                     // :89-92

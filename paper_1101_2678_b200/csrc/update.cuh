@@ -478,43 +478,46 @@ __global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
 // candidate set overflows the scratch is marked invalid (entry 0 = -2) and
 // always scans.  Rebuilt after every choice_info recomputation.
 //
-// Per row (one 256-thread CTA): the row is staged in shared memory; 512
-// strided sub-range maxima; M = the KT-th largest of them (by rank), so at
-// least KT cities have w >= M; those cities are collected and ranked by the
-// total order.  Bytes: 8 n^2 read + 4 KT n written.
+// Per row (one 256-thread CTA): 256 strided sub-range maxima straight from
+// the row (8 loads in flight per thread); M = the KT-th largest of them (by
+// rank), so at least KT cities have w >= M; a second pass over the row (L2-
+// resident by then) collects those cities, which are ranked by the total
+// order.  Bytes: 8 n^2 from HBM (+ the L2 re-read) + 4 KT n written.
 constexpr int kTopK = 128;
 constexpr int kTopCap = 768;
 
 __global__ void __launch_bounds__(256) k_row_topk(const double* __restrict__ choice, int n, int P64,
                                                   int32_t* __restrict__ topk) {
-    extern __shared__ double tk_smem[];
-    double* row = tk_smem;                 // P64
-    double* smax = row + P64;              // 512
-    double* cv = smax + 512;               // kTopCap
-    int* ci = reinterpret_cast<int*>(cv + kTopCap); // kTopCap
+    __shared__ double smax[256];
+    __shared__ double cv[kTopCap];
+    __shared__ int ci[kTopCap];
     __shared__ int s_cnt;
     __shared__ double s_min[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int B = 8; // loads in flight per thread
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
         const double* src = choice + static_cast<size_t>(i) * P64;
-        for (int j = tid; j < n; j += 256) row[j] = src[j];
         if (tid == 0) s_cnt = 0;
-        __syncthreads();
+        // sub-range q = j mod 256 is thread q's: its maximum straight from HBM
+        double m0 = -1.0;
+        for (int k0 = 0; k0 < n; k0 += 256 * B) {
+            double v[B];
 #pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const int q = tid + 256 * s;
-            double mx = -1.0;
-            for (int j = q; j < n; j += 512) mx = fmax(mx, row[j]);
-            smax[q] = mx;
+            for (int u = 0; u < B; ++u) {
+                const int j = k0 + 256 * u + tid;
+                v[u] = j < n ? __ldg(src + j) : -1.0;
+            }
+#pragma unroll
+            for (int u = 0; u < B; ++u) m0 = fmax(m0, v[u]);
         }
+        smax[tid] = m0;
         __syncthreads();
+        // M = the KT-th largest sub-range maximum: >= KT cities have w >= M
         double mine = 1e308;
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const double v = smax[tid + 256 * s];
+        {
             int r = 0;
-            for (int q = 0; q < 512; ++q) r += smax[q] > v ? 1 : 0;
-            if (r < kTopK && v >= 0.0) mine = fmin(mine, v);
+            for (int q = 0; q < 256; ++q) r += smax[q] > m0 ? 1 : 0;
+            if (r < kTopK && m0 >= 0.0) mine = m0;
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) mine = fmin(mine, __shfl_xor_sync(kFull, mine, off));
@@ -522,13 +525,22 @@ __global__ void __launch_bounds__(256) k_row_topk(const double* __restrict__ cho
         __syncthreads();
         double M = s_min[0];
         for (int w = 1; w < 8; ++w) M = fmin(M, s_min[w]);
-        for (int j = tid; j < n; j += 256) {
-            const double v = row[j];
-            if (v >= M) {
-                const int pos = atomicAdd(&s_cnt, 1);
-                if (pos < kTopCap) {
-                    cv[pos] = v;
-                    ci[pos] = j;
+        // second pass over the (now L2-resident) row: collect w >= M
+        for (int k0 = 0; k0 < n; k0 += 256 * B) {
+            double v[B];
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                const int j = k0 + 256 * u + tid;
+                v[u] = j < n ? __ldg(src + j) : -1.0;
+            }
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                if (v[u] >= M) {
+                    const int pos = atomicAdd(&s_cnt, 1);
+                    if (pos < kTopCap) {
+                        cv[pos] = v[u];
+                        ci[pos] = k0 + 256 * u + tid;
+                    }
                 }
             }
         }
