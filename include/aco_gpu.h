@@ -99,7 +99,9 @@ typedef struct {
     int32_t device;       /* CUDA device ordinal */
     /* Ant sharding: this context constructs global ants
      * [ant_begin, ant_end) of m; 0/0 means all.  With world > 1 the
-     * per-iteration exchange runs over NCCL (nccl_id from rank 0). */
+     * per-iteration exchange runs over NCCL (nccl_id from rank 0, one id
+     * per context).  world == 1 with a non-zero nccl_id runs the same
+     * sharded protocol on a one-rank communicator. */
     int32_t rank, world;
     int32_t ant_begin, ant_end;
     uint8_t nccl_id[128];

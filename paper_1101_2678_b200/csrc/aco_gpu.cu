@@ -132,6 +132,7 @@ struct aco_gpu_ctx {
     long long* h_stats = nullptr;       // pinned: 4 stats + 2 fallback counters
     ncclComm_t comm = nullptr;
     bool external = false; // world > 1 without an NCCL id: the caller exchanges
+    bool sharded = false;  // the sharded protocol (world > 1, or a 1-rank NCCL communicator)
 };
 
 namespace {
@@ -347,7 +348,7 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
     rp.LA = c->LA;
     rp.shards = c->world;
     rp.S = c->S;
-    rp.m = c->world == 1 ? c->mloc : c->m; // a local ant range is one shard of mloc ants
+    rp.m = !c->sharded ? c->mloc : c->m; // a local ant range is one shard of mloc ants
     rp.alpha = c->cfg.alpha;
     rp.keep = 1.0 - c->cfg.rho; // pheromone.hpp:179
     const size_t smem = static_cast<size_t>(c->P64) * sizeof(double);
@@ -513,12 +514,12 @@ void do_construct(aco_gpu_ctx* c) {
             c->d_inv + static_cast<size_t>(c->rank) * c->S, succ, pred, c->S);
         check_launch(c, "k_tour_length");
     }
-    // world == 1: stats kernel also maintains best-so-far on device.
+    // unsharded: the stats kernel also maintains best-so-far on device.
     k_iter_stats<<<1, 1024, 0, c->stream>>>(
         c->d_len, c->mloc, c->d_tours, c->n, c->d_stats, c->d_stats + 3, c->d_best,
-        c->world == 1 ? 1 : 0);
+        c->sharded ? 0 : 1);
     check_launch(c, "k_iter_stats");
-    if (c->world > 1 && !gather_mode(c)) { // local delta for the all-reduce
+    if (c->sharded && !gather_mode(c)) { // local delta for the all-reduce
         k_deposit_atomic<<<c->num_sms * 8, 256, 0, c->stream>>>(
             c->d_tours, c->d_inv + static_cast<size_t>(c->rank) * c->S, c->n, c->P64, c->mloc,
             c->d_delta);
@@ -530,7 +531,7 @@ void do_construct(aco_gpu_ctx* c) {
 // exchange + evaporate + deposit + choice (no host sync)
 void do_update(aco_gpu_ctx* c) {
     const double keep = 1.0 - c->cfg.rho;
-    if (c->world > 1 && !c->external) {
+    if (c->sharded && !c->external) {
         auto& api = nccl();
         if (gather_mode(c)) {
             const size_t blk = static_cast<size_t>(c->n) * c->S;
@@ -549,7 +550,7 @@ void do_update(aco_gpu_ctx* c) {
     if (gather_mode(c)) {
         launch_rows(c, MODE_GATHER);
         CK(cudaEventRecord(c->ev[4], c->stream));
-    } else if (c->world > 1) {
+    } else if (c->sharded) {
         launch_rows(c, MODE_DELTA);
         CK(cudaEventRecord(c->ev[4], c->stream));
     } else {
@@ -574,7 +575,7 @@ float ev_ms(aco_gpu_ctx* c, int a, int b) {
 // Reads stats; for world > 1 reduces them over NCCL (best, then owner, sum)
 // and broadcasts the improving tour.
 void finish_stats(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
-    if (c->world > 1 && !c->external) {
+    if (c->sharded && !c->external) {
         auto& api = nccl();
         long long* s = c->d_stats;
         // s[0] best len (local), s[1] best local ant, s[2] sum.
@@ -739,6 +740,17 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         }
         c->mloc = c->ant_end - c->ant_begin;
         c->device = prm->device;
+        {
+            // world > 1 with a zero id: external exchange (the caller runs
+            // the collectives); world == 1 with an id: the sharded protocol on
+            // a one-rank NCCL communicator (exercises the exchange path)
+            bool zero = true;
+            for (int i = 0; i < 128; ++i) zero = zero && prm->nccl_id[i] == 0;
+            c->sharded = c->world > 1 || !zero;
+            c->external = c->world > 1 && zero;
+            if (c->world == 1 && !zero && (prm->ant_begin != 0 || prm->ant_end != 0))
+                throw ModelError(Errc::config_error, "an ant range and an NCCL id exclude each other");
+        }
 
         // host model: distances, eta^beta table, tau0, nn lists
         const int n = c->n;
@@ -825,7 +837,7 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
             CK(cudaMalloc(&c->d_pred, sp * sizeof(int32_t)));
             CK(cudaMemset(c->d_succ, 0, sp * sizeof(int32_t)));
             CK(cudaMemset(c->d_pred, 0, sp * sizeof(int32_t)));
-        } else if (c->world > 1) {
+        } else if (c->sharded) {
             CK(cudaMalloc(&c->d_delta, cells * sizeof(double)));
             CK(cudaMemset(c->d_delta, 0, cells * sizeof(double)));
         }
@@ -841,12 +853,7 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
 #endif
         CK(cudaMallocHost(&c->h_stats, 8 * sizeof(long long)));
 
-        if (c->world > 1) {
-            bool zero = true;
-            for (int i = 0; i < 128; ++i) zero = zero && prm->nccl_id[i] == 0;
-            c->external = zero;
-        }
-        if (c->world > 1 && !c->external) {
+        if (c->sharded && !c->external) {
             auto& api = nccl();
             if (!api.CommInitRank) throw Fail{ACO_E_NCCL, "libnccl.so.2 not found"};
             ncclUniqueId id;
@@ -981,7 +988,7 @@ aco_status aco_gpu_update(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
         if (rec) {
             rec->update_ms = ev_ms(c, 2, 5);
             rec->exchange_ms = ev_ms(c, 2, 3);
-            rec->choice_ms = (!gather_mode(c) && c->world == 1) ? ev_ms(c, 4, 5) : 0.0;
+            rec->choice_ms = (!gather_mode(c) && !c->sharded) ? ev_ms(c, 4, 5) : 0.0;
         }
         ++c->iteration;
     });
@@ -995,7 +1002,7 @@ aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* to
         aco_gpu_iter_record* r = rec ? rec : &tmp;
         fill_common(c, r);
         do_construct(c);
-        if (c->world > 1 && !c->external) {
+        if (c->sharded && !c->external) {
             // stats must be reduced before the best tour can be broadcast
             CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
             finish_stats(c, r);
@@ -1013,17 +1020,17 @@ aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* to
                                    cudaMemcpyDeviceToHost, c->copy_stream));
         }
         do_update(c);
-        if (c->world == 1 || c->external)
+        if (!c->sharded || c->external)
             CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(c->h_stats + 6, c->d_fb, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         if (tours_out || lengths_out) CK(cudaStreamSynchronize(c->copy_stream));
-        if (c->world == 1 || c->external) finish_stats(c, r);
+        if (!c->sharded || c->external) finish_stats(c, r);
         r->construct_ms = ev_ms(c, 0, 2);
         r->construct_kernel_ms = ev_ms(c, 0, 1);
         r->update_ms = ev_ms(c, 2, 5);
         r->exchange_ms = ev_ms(c, 2, 3);
-        r->choice_ms = (!gather_mode(c) && c->world == 1) ? ev_ms(c, 4, 5) : 0.0;
+        r->choice_ms = (!gather_mode(c) && !c->sharded) ? ev_ms(c, 4, 5) : 0.0;
         r->fallbacks = c->h_stats[6] + c->h_stats[7];
         c->last_fb[0] = c->h_stats[6];
         c->last_fb[1] = c->h_stats[7];

@@ -89,3 +89,41 @@ def test_virtual_shards_match_single_context(deposit, G, m):
                 e.set_pheromone(tau_ref)
     for e in shards + [single]:
         e.close()
+
+
+@pytest.mark.parametrize("deposit", [1, 0])
+def test_nccl_exchange_path_one_rank(deposit):
+    """The NCCL exchange path (all-gather of succ/pred/1/C_k, or all-reduce of
+    the local delta + k_rows<DELTA>; NCCL reduction of the statistics and
+    broadcast of the best tour) on a one-rank communicator: tours, best
+    tour and statistics equal the unsharded engine's; tau bit-exact on the
+    gather path and within 1e-5 relative on the atomic path."""
+    from paper_1101_2678_b200 import aco
+
+    n = 300
+    prob = aco.build_problem(aco.synthetic_instance(n))
+
+    def cfg(nccl_id=None):
+        return aco.RunConfig(params=aco.Parameters(m=0, seed=2),
+                             selection=aco.SelectionStrategy(aco.Selection.roulette_full),
+                             deposit=aco.DepositStrategy(aco.Deposit(deposit)), nccl_id=nccl_id)
+
+    plain = aco.Engine(prob, cfg())
+    nccl = aco.Engine(prob, cfg(aco.nccl_unique_id()))
+    for it in range(4):
+        ra = plain.run_iteration()
+        rb = nccl.run_iteration()
+        ta, la = plain.ants()
+        tb, lb = nccl.ants()
+        assert np.array_equal(ta, tb), f"tours differ at iteration {it}"
+        assert ra.best_length == rb.best_length and ra.mean_length == rb.mean_length
+        assert plain.best_length() == nccl.best_length()
+        assert np.array_equal(plain.best_tour(), nccl.best_tour())
+        pa, pb = plain.pheromone(), nccl.pheromone()
+        if deposit != 0:
+            assert np.array_equal(pa, pb)
+        else:
+            assert (np.abs(pa - pb) / pa).max() <= 1e-5
+            nccl.set_pheromone(pa)  # keep the construction inputs identical
+    plain.close()
+    nccl.close()
