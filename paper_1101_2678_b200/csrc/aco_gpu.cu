@@ -129,7 +129,8 @@ struct aco_gpu_ctx {
     int32_t* d_best = nullptr;      // n+1
     unsigned long long* d_fb = nullptr; // [0] roulette fallbacks, [1] nn argmax fallbacks
     unsigned long long* d_timing = nullptr; // ACO_TIMING phase cycles
-    long long* h_stats = nullptr;       // pinned: 4 stats + 2 fallback counters
+    long long* h_stats = nullptr;       // pinned: [0..7] d_stats, [8..9] fallback counters
+    int32_t* d_tourbuf = nullptr;       // sharded: winning tour exchange buffer (n+1)
     ncclComm_t comm = nullptr;
     bool external = false; // world > 1 without an NCCL id: the caller exchanges
     bool sharded = false;  // the sharded protocol (world > 1, or a 1-rank NCCL communicator)
@@ -572,42 +573,35 @@ float ev_ms(aco_gpu_ctx* c, int a, int b) {
     return ms;
 }
 
-// Reads stats; for world > 1 reduces them over NCCL (best, then owner, sum)
-// and broadcasts the improving tour.
+// Sharded (NCCL) statistics, enqueued on the engine stream with no host
+// synchronisation: key MIN + sum SUM all-reduces, the owner's tour
+// replicated by an all-reduce MAX, best-so-far updated on the device.
+void enqueue_shard_stats(aco_gpu_ctx* c) {
+    auto& api = nccl();
+    long long* s = c->d_stats;
+    k_shard_key<<<1, 32, 0, c->stream>>>(s, c->ant_begin, c->mloc);
+    check_launch(c, "k_shard_key");
+    NK(api.GroupStart());
+    NK(api.AllReduce(s + 4, s + 4, 1, ncclInt64, ncclMin, c->comm, c->stream));
+    NK(api.AllReduce(s + 6, s + 6, 1, ncclInt64, ncclSum, c->comm, c->stream));
+    NK(api.GroupEnd());
+    k_owner_tour<<<std::max(1, (c->n + 256) / 256), 256, 0, c->stream>>>(
+        s, c->d_tours, c->n, c->ant_begin, c->ant_end, c->d_tourbuf);
+    check_launch(c, "k_owner_tour");
+    NK(api.AllReduce(c->d_tourbuf, c->d_tourbuf, c->n + 1, ncclInt32, ncclMax, c->comm, c->stream));
+    k_best_update<<<1, 1024, 0, c->stream>>>(s, c->d_tourbuf, c->n, c->d_best);
+    check_launch(c, "k_best_update");
+}
+
+// Fills the record from h_stats[0..7] (copied from d_stats after the stream
+// synchronised).  Sharded: the reduced key / sum and the device best-so-far;
+// otherwise (and in external mode) this shard's own statistics.
 void finish_stats(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
     if (c->sharded && !c->external) {
-        auto& api = nccl();
-        long long* s = c->d_stats;
-        // s[0] best len (local), s[1] best local ant, s[2] sum.
-        // scratch: s[4] global best, s[5] owner key, s[6] global sum
-        CK(cudaMemcpyAsync(s + 4, s, sizeof(long long), cudaMemcpyDeviceToDevice, c->stream));
-        CK(cudaMemcpyAsync(s + 6, s + 2, sizeof(long long), cudaMemcpyDeviceToDevice, c->stream));
-        NK(api.GroupStart());
-        NK(api.AllReduce(s + 4, s + 4, 1, ncclInt64, ncclMin, c->comm, c->stream));
-        NK(api.AllReduce(s + 6, s + 6, 1, ncclInt64, ncclSum, c->comm, c->stream));
-        NK(api.GroupEnd());
-        CK(cudaMemcpyAsync(c->h_stats, s, 7 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        const long long gbest = c->h_stats[4];
-        long long key = c->h_stats[0] == gbest ? c->ant_begin + c->h_stats[1] : LLONG_MAX;
-        CK(cudaMemcpyAsync(s + 5, &key, sizeof(long long), cudaMemcpyHostToDevice, c->stream));
-        NK(api.AllReduce(s + 5, s + 5, 1, ncclInt64, ncclMin, c->comm, c->stream));
-        CK(cudaMemcpyAsync(c->h_stats + 5, s + 5, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        const long long owner_ant = c->h_stats[5];
-        const int owner = static_cast<int>(owner_ant / c->S);
-        rec->best_length = gbest;
+        rec->best_length = c->h_stats[4] >> 24;
         rec->mean_length = static_cast<double>(c->h_stats[6]) / static_cast<double>(c->m);
-        if (gbest < c->best_so_far) {
-            c->best_so_far = gbest;
-            if (c->rank == owner) {
-                const int local = static_cast<int>(owner_ant - c->ant_begin);
-                CK(cudaMemcpyAsync(c->d_best, c->d_tours + static_cast<size_t>(local) * (c->n + 1),
-                                   sizeof(int32_t) * (c->n + 1), cudaMemcpyDeviceToDevice, c->stream));
-            }
-            NK(api.Broadcast(c->d_best, c->d_best, c->n + 1, ncclInt32, owner, c->comm, c->stream));
-        }
-    } else { // one shard (external mode: this shard's own statistics)
+        c->best_so_far = c->h_stats[3];
+    } else {
         rec->best_length = c->h_stats[0];
         rec->mean_length = static_cast<double>(c->h_stats[2]) / static_cast<double>(c->mloc);
         c->best_so_far = std::min<int64_t>(c->best_so_far, c->h_stats[0]);
@@ -851,7 +845,11 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         CK(cudaMalloc(&c->d_timing, 8 * sizeof(unsigned long long)));
         CK(cudaMemset(c->d_timing, 0, 8 * sizeof(unsigned long long)));
 #endif
-        CK(cudaMallocHost(&c->h_stats, 8 * sizeof(long long)));
+        CK(cudaMallocHost(&c->h_stats, 16 * sizeof(long long)));
+        if (c->sharded) {
+            if (c->m >= (1 << 24)) throw Fail{ACO_E_UNSUPPORTED, "sharded colonies support m < 2^24 ants"};
+            CK(cudaMalloc(&c->d_tourbuf, (n + 1) * sizeof(int32_t)));
+        }
 
         if (c->sharded && !c->external) {
             auto& api = nccl();
@@ -898,7 +896,7 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
     if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
     void* bufs[] = {c->d_choice_nn, c->d_topk, c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
                     c->d_choice_p64, c->d_scale, c->d_nn, c->d_tours, c->d_len, c->d_inv,
-                    c->d_succ, c->d_pred, c->d_delta, c->d_stats, c->d_best, c->d_fb};
+                    c->d_succ, c->d_pred, c->d_delta, c->d_stats, c->d_best, c->d_fb, c->d_tourbuf};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_stats) cudaFreeHost(c->h_stats);
@@ -963,12 +961,13 @@ aco_status aco_gpu_construct(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
     return guard_ctx(c, [&] {
         CK(cudaSetDevice(c->device));
         do_construct(c);
-        CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(c->h_stats + 6, c->d_fb, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        if (c->sharded && !c->external) enqueue_shard_stats(c);
+        CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 8 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h_stats + 8, c->d_fb, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         aco_gpu_iter_record tmp{};
         aco_gpu_iter_record* r = rec ? rec : &tmp;
-        const long long fb0 = c->h_stats[6], fb1 = c->h_stats[7];
+        const long long fb0 = c->h_stats[8], fb1 = c->h_stats[9];
         c->last_fb[0] = fb0;
         c->last_fb[1] = fb1;
         fill_common(c, r);
@@ -1002,11 +1001,9 @@ aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* to
         aco_gpu_iter_record* r = rec ? rec : &tmp;
         fill_common(c, r);
         do_construct(c);
-        if (c->sharded && !c->external) {
-            // stats must be reduced before the best tour can be broadcast
-            CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-            finish_stats(c, r);
-        }
+        // sharded: statistics and best tour reduced on the device, in stream
+        // order before the update (no host round trip inside the iteration)
+        if (c->sharded && !c->external) enqueue_shard_stats(c);
         // the tours are final once the construction phase (ev[2]) is done:
         // copy them out on a second stream while the update runs (the update
         // only reads them), and join before returning
@@ -1020,20 +1017,19 @@ aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* to
                                    cudaMemcpyDeviceToHost, c->copy_stream));
         }
         do_update(c);
-        if (!c->sharded || c->external)
-            CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 4 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(c->h_stats + 6, c->d_fb, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 8 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h_stats + 8, c->d_fb, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         if (tours_out || lengths_out) CK(cudaStreamSynchronize(c->copy_stream));
-        if (!c->sharded || c->external) finish_stats(c, r);
+        finish_stats(c, r);
         r->construct_ms = ev_ms(c, 0, 2);
         r->construct_kernel_ms = ev_ms(c, 0, 1);
         r->update_ms = ev_ms(c, 2, 5);
         r->exchange_ms = ev_ms(c, 2, 3);
         r->choice_ms = (!gather_mode(c) && !c->sharded) ? ev_ms(c, 4, 5) : 0.0;
-        r->fallbacks = c->h_stats[6] + c->h_stats[7];
-        c->last_fb[0] = c->h_stats[6];
-        c->last_fb[1] = c->h_stats[7];
+        r->fallbacks = c->h_stats[8] + c->h_stats[9];
+        c->last_fb[0] = c->h_stats[8];
+        c->last_fb[1] = c->h_stats[9];
         r->best_so_far = c->best_so_far;
         ++c->iteration;
     });

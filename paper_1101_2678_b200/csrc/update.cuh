@@ -118,6 +118,42 @@ __global__ void __launch_bounds__(1024) k_iter_stats(const int64_t* __restrict__
     }
 }
 
+// Sharded statistics entirely on the device (no host round trip between
+// the construction and the update).  Stage 1, before the MIN / SUM
+// all-reduces: key = (best length << 24) | global ant, so the MIN gives the
+// iteration best AND its lowest global ant (engine.hpp:117-129 tie rule).
+__global__ void k_shard_key(long long* stats, int ant_begin, int mloc) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        stats[4] = mloc > 0 ? (stats[0] << 24) | static_cast<long long>(ant_begin + stats[1])
+                            : LLONG_MAX;
+        stats[6] = stats[2];
+    }
+}
+// Stage 2, after them: the rank owning the winning ant copies its tour into
+// the exchange buffer, the others zero it; an all-reduce MAX replicates it
+// (tour entries are >= 0).
+__global__ void k_owner_tour(const long long* __restrict__ stats, const int32_t* __restrict__ tours,
+                             int n, int ant_begin, int ant_end, int32_t* __restrict__ tourbuf) {
+    const long long key = stats[4];
+    const int ant = static_cast<int>(key & 0xFFFFFF);
+    const bool own = key != LLONG_MAX && ant >= ant_begin && ant < ant_end;
+    const int32_t* src = tours + static_cast<size_t>(own ? ant - ant_begin : 0) * (n + 1);
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s <= n; s += gridDim.x * blockDim.x)
+        tourbuf[s] = own ? src[s] : 0;
+}
+// Stage 3: best-so-far and its tour on strict improvement (engine.hpp:151-154).
+__global__ void __launch_bounds__(1024) k_best_update(long long* stats, const int32_t* __restrict__ tourbuf,
+                                                      int n, int32_t* __restrict__ best_tour) {
+    __shared__ int imp;
+    const long long gl = stats[4] >> 24;
+    if (threadIdx.x == 0) imp = gl < stats[3];
+    __syncthreads();
+    if (imp)
+        for (int s = threadIdx.x; s <= n; s += blockDim.x) best_tour[s] = tourbuf[s];
+    __syncthreads();
+    if (threadIdx.x == 0 && imp) stats[3] = gl;
+}
+
 __global__ void k_evaporate(double* __restrict__ tau, size_t count2, double keep) {
     double2* t2 = reinterpret_cast<double2*>(tau);
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count2;
