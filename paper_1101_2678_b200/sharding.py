@@ -11,12 +11,17 @@ engine (aco_gpu.cu: aco_gpu_create / do_update / finish_stats) implements.
 * Atomic deposit: each rank scatters its ants into a zeroed delta, delta is
   all-reduced (sum), then tau = fl(fl(tau * (1 - rho)) + delta) — within the
   1e-5 relative tolerance of deposit_accumulate (pheromone.hpp:195-208).
-* Iteration stats: all-reduce MIN of the best length, then MIN of the global
-  ant index among the ranks holding it (the reference's lowest-index tie
-  rule, engine.hpp:117-129), all-reduce SUM of the int64 lengths; the owner
-  broadcasts the best tour when it strictly improves best-so-far.
+* Iteration stats, all on the device (no host round trip): one all-reduce
+  MIN of the packed key (best length << 24 | global ant) gives the best
+  length and its lowest global ant (the reference's tie rule,
+  engine.hpp:117-129); all-reduce SUM of the int64 lengths; the owning rank
+  contributes its best tour and the others zeros to an all-reduce MAX,
+  which replicates the winning tour; best-so-far updates on strict
+  improvement (engine.hpp:151-154).
 """
 from __future__ import annotations
+
+KEY_SHIFT = 24  # global ant ids < 2**24
 
 
 def shard_size(m: int, world: int) -> int:
@@ -30,3 +35,13 @@ def shard_range(m: int, world: int, rank: int):
 
 def owner_of(ant: int, m: int, world: int) -> int:
     return ant // shard_size(m, world)
+
+
+def stats_key(best_length: int, best_local_ant: int, ant_begin: int) -> int:
+    """Packed MIN key of a shard's iteration best (k_shard_key)."""
+    return (best_length << KEY_SHIFT) | (ant_begin + best_local_ant)
+
+
+def unpack_key(key: int):
+    """(best length, global ant) of a reduced key."""
+    return key >> KEY_SHIFT, key & ((1 << KEY_SHIFT) - 1)

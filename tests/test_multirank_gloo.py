@@ -25,7 +25,8 @@ def _worker(rank, world, port, n, m, iters, out_path):
 
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from paper_1101_2678_b200.sharding import owner_of, shard_range, shard_size
+    from paper_1101_2678_b200.sharding import (owner_of, shard_range, shard_size, stats_key,
+                                              unpack_key)
     from pyoracle import Oracle, synth_coords
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
@@ -43,17 +44,20 @@ def _worker(rank, world, port, n, m, iters, out_path):
         # construction of the local shard, global ant ids
         tg, lg, _ = O.construct(d, O.choice(d, tau_g), 1, it, a0, a1)
         ta, la, _ = O.construct(d, O.choice(d, tau_a), 1, it, a0, a1)
-        # stats: min len, then min global owner ant among holders, sum
-        loc_best = int(lg.min()) if len(lg) else 2**62
-        t = torch.tensor([loc_best], dtype=torch.int64)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        gbest = int(t.item())
-        key = a0 + int(np.argmin(lg)) if loc_best == gbest else 2**62
-        k = torch.tensor([key], dtype=torch.int64)
-        dist.all_reduce(k, op=dist.ReduceOp.MIN)
+        # stats: packed (length << 24 | global ant) MIN, length SUM (k_shard_key)
+        key = stats_key(int(lg.min()), int(np.argmin(lg)), a0) if len(lg) else 2**63 - 1
+        kt = torch.tensor([key], dtype=torch.int64)
+        dist.all_reduce(kt, op=dist.ReduceOp.MIN)
+        gbest, gant = unpack_key(int(kt.item()))
+        k = torch.tensor([gant], dtype=torch.int64)
         s = torch.tensor([int(lg.sum())], dtype=torch.int64)
         dist.all_reduce(s, op=dist.ReduceOp.SUM)
-        assert owner_of(int(k.item()), m, world) in range(world)
+        assert owner_of(gant, m, world) in range(world)
+        # the owner's tour, replicated by an all-reduce MAX (k_owner_tour)
+        tb = torch.from_numpy(tg[gant - a0].copy() if a0 <= gant < a1
+                              else np.zeros(n + 1, np.int32))
+        dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+        best_tour = tb.numpy().copy()
         # gather path: all-gather tours (shard-major, padded to S) then fold in order
         pad = np.full((S, n + 1), -1, np.int32)
         pad[: a1 - a0] = tg
@@ -71,6 +75,7 @@ def _worker(rank, world, port, n, m, iters, out_path):
         dt = torch.from_numpy(delta)
         dist.all_reduce(dt, op=dist.ReduceOp.SUM)
         tau_a = tau_a * 0.5 + dt.numpy()
+        assert np.array_equal(best_tour, tours[gant])
         trace.append((gbest, int(k.item()), int(s.item()), tours))
     if rank == 0:
         np.savez(out_path, tau_g=tau_g, tau_a=tau_a,
