@@ -92,6 +92,7 @@ struct aco_gpu_ctx {
     int P64 = 0, PW = 0, NV = 0, V = 4, C = 0, R = 1, MAXR = 1, tabu_words = 0;
     int LA = 32;          // lanes sharing a streamed row (16: two ants per warp)
     int team = 1;         // warps per ant (k_construct_team when > 1)
+    bool exact_only = false; // k_construct_roulette_exact (rows too long to stream)
     int half_smem = 0;    // pair kernel: bytes per half
     double tau0 = 0.0;
     int64_t max_d = 0;
@@ -304,10 +305,18 @@ void choose_stream_layout(aco_gpu_ctx* c) {
         c->NV = 20;
         c->MAXR = 8;
         c->R = (c->n + 32 * 20 * c->V - 1) / (32 * 20 * c->V);
-        if (c->R > 8)
-            throw Fail{ACO_E_UNSUPPORTED, "full-row roulette supports n <= " +
-                                              std::to_string(8 * 32 * 20 * c->V) +
-                                              " with this weight stream"};
+    }
+    const char* ex = std::getenv("ACO_ROULETTE_EXACT");
+    if (c->cfg.selection == ACO_SEL_ROULETTE && (c->R > 8 || (ex && ex[0] == '1'))) {
+        // rows too long for the streamed layouts: exact replay every step
+        c->exact_only = true;
+        c->NV = 20;
+        c->MAXR = 8;
+        c->R = 1;
+        c->C = c->NV * c->V;
+        c->PW = 0;
+        c->tabu_words = (c->n + 31) / 32 + 2;
+        return;
     }
     c->C = c->NV * c->V;
     c->PW = c->R * kLP * c->C;        // physical row length (with pad slots)
@@ -436,6 +445,19 @@ void launch_construct(aco_gpu_ctx* c) {
             std::fprintf(stderr, "construct: %s\n", c->construct_desc.c_str());
         fn<<<grid, 32, smem, c->stream>>>(p);
         check_launch(c, "k_construct_roulette_pair");
+    } else if (c->cfg.selection == ACO_SEL_ROULETTE && c->exact_only) {
+        const uint32_t stage_bytes = 16 * 1024;
+        const size_t smem = 128 + stage_bytes + smem1 + static_cast<size_t>((c->n + 31) / 32) * sizeof(double) + 8;
+        if (smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(k_construct_roulette_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_construct_roulette_exact, 32, smem));
+        const int grid = std::max(1, std::min(c->mloc, std::max(1, per_sm) * c->num_sms));
+        c->construct_grid = grid;
+        c->construct_desc = "k_construct_roulette_exact grid=" + std::to_string(grid);
+        k_construct_roulette_exact<<<grid, 32, smem, c->stream>>>(p, stage_bytes);
+        check_launch(c, "k_construct_roulette_exact");
     } else if (c->cfg.selection == ACO_SEL_ROULETTE && c->team > 1) {
         ConstructFn fn = pick_team(c->team, c->NV);
         const size_t smem = 256 + static_cast<size_t>(c->PW) * 4 + smem1 +
@@ -798,7 +820,7 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         CK(cudaMalloc(&c->d_choice, cells * sizeof(double)));
         CK(cudaMemset(c->d_choice, 0, cells * sizeof(double)));
         const size_t wcells = static_cast<size_t>(n) * c->PW;
-        if (c->cfg.selection == ACO_SEL_ROULETTE) {
+        if (c->cfg.selection == ACO_SEL_ROULETTE && c->PW > 0) {
             if (c->stream_kind == ACO_STREAM_FP32) {
                 CK(cudaMalloc(&c->d_choice32, wcells * sizeof(float)));
                 CK(cudaMemset(c->d_choice32, 0, wcells * sizeof(float)));

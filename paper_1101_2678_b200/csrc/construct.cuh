@@ -857,6 +857,58 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
 }
 
 // ---------------------------------------------------------------------------
+// Full-row roulette for rows too long for the streamed-row layouts (n beyond
+// 8 rounds of 32 lanes x 80 cities) or on request (ACO_ROULETTE_EXACT=1):
+// every step is the exact replay of select_next_roulette (exact_walk: the
+// fp64 row staged through shared memory in TMA pieces, every lane folding
+// every weight in ascending order).  Slower, but any n.
+__global__ void __launch_bounds__(32) k_construct_roulette_exact(ConstructParams p, uint32_t stage_bytes) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    double* stage = reinterpret_cast<double*>(smem_raw + 128);
+    uint32_t* tabu = reinterpret_cast<uint32_t*>(smem_raw + 128 + stage_bytes);
+    double* chunk_start = reinterpret_cast<double*>(tabu + p.tabu_words);
+    const int lane = threadIdx.x & 31;
+    const int n = p.n;
+    if (lane == 0) mbar_init(bar, 1);
+    __syncwarp();
+    uint32_t phase = 0;
+    const uint32_t flip = static_cast<uint32_t>(exact_walk_pieces(n, stage_bytes) & 1);
+    for (int kl = blockIdx.x; kl < p.mloc; kl += gridDim.x) {
+        const uint32_t kg = static_cast<uint32_t>(p.ant_begin + kl);
+        int32_t* tour = p.tours + static_cast<size_t>(kl) * (n + 1);
+        tabu_init(tabu, p.tabu_words, n, lane);
+        const int start = start_city(p, kg);
+        __syncwarp();
+        if (lane == 0) {
+            tabu[start >> 5] |= 1u << (start & 31);
+            tour[0] = start;
+        }
+        __syncwarp();
+        int cur = start;
+        double ubatch = 0.0;
+        for (int step = 1; step < n; ++step) {
+            if (((step - 1) & 31) == 0)
+                ubatch = philox_uniform(p.seed, p.iteration, kg, static_cast<uint32_t>(step + lane), 0);
+            const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
+            const int next = exact_walk(p.w64 + static_cast<size_t>(cur) * p.P64, tabu, n,
+                                        p.tabu_words, u, lane, chunk_start, stage, stage_bytes, bar,
+                                        phase);
+            phase ^= flip;
+            __syncwarp();
+            if (lane == 0) {
+                tabu[next >> 5] |= 1u << (next & 31);
+                tour[step] = next;
+            }
+            __syncwarp();
+            cur = next;
+        }
+        if (lane == 0) tour[n] = start;
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // NN-list roulette (select_next_nn, construction.hpp:73-121).  Lane q holds
 // list member q (nn <= 32 per pass) and its fp64 weight (0 if visited).  One
 // fold over the list: every lane adds the broadcast weights in LIST order —

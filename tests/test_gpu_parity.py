@@ -357,3 +357,38 @@ def test_small_and_degenerate_instances_bit_exact(aco, oracle, n, selection, dup
             assert np.array_equal(l, l_ref)
             tau = oracle.update(tau, t_ref, l_ref, 0.5, 1)
             assert np.array_equal(eng.pheromone(), tau)
+
+
+def test_roulette_exact_kernel_forced_bit_exact(aco, oracle, monkeypatch):
+    """k_construct_roulette_exact (every step the exact replay) forced at
+    n = 1002: tours and the gather tau bit-exact over two iterations."""
+    monkeypatch.setenv("ACO_ROULETTE_EXACT", "1")
+    n = 1002
+    prob, eng = make(aco, n, deposit=1)
+    with eng:
+        tau = np.full((n, n), eng.tau0)
+        for it in range(2):
+            ch = oracle.choice(prob.dist, tau)
+            eng.run_iteration()
+            assert "k_construct_roulette_exact" in eng.describe()
+            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, 0, n)
+            t, l = eng.ants()
+            assert np.array_equal(t, t_ref), f"iteration {it}"
+            tau = oracle.update(tau, t_ref, l_ref, 0.5, 1)
+            assert np.array_equal(eng.pheromone(), tau)
+
+
+def test_roulette_beyond_streamed_layout_limit(aco, oracle):
+    """n beyond the streamed layouts (fp64 stream: 8 rounds x 32 lanes x 40
+    cities = 10240) falls back to the exact-replay kernel instead of failing:
+    n = 10300, four ants, tours bit-exact against the oracle."""
+    n, m = 10300, 4
+    prob, eng = make(aco, n, stream=1, m=m)
+    with eng:
+        eng.construct()
+        assert "k_construct_roulette_exact" in eng.describe()
+        t, l = eng.ants()
+        tau = np.full((n, n), eng.tau0)
+        t_ref, l_ref, _ = oracle.construct(prob.dist, oracle.choice(prob.dist, tau), 1, 0, 0, m)
+        assert np.array_equal(t, t_ref)
+        assert np.array_equal(l, l_ref)
