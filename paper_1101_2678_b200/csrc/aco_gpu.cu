@@ -20,7 +20,6 @@
 
 #include "../../include/aco_gpu.h"
 #include "construct.cuh"
-#include "construct_pair.cuh"
 #include "construct_team.cuh"
 #include "host_model.hpp"
 #include "update.cuh"
@@ -90,10 +89,9 @@ struct aco_gpu_ctx {
     int random_start = 0;
     int rank = 0, world = 1, ant_begin = 0, ant_end = 0, mloc = 0, S = 0;
     int P64 = 0, PW = 0, NV = 0, V = 4, C = 0, R = 1, MAXR = 1, tabu_words = 0;
-    int LA = 32;          // lanes sharing a streamed row (16: two ants per warp)
+    int LA = 32;          // lanes sharing a streamed row
     int team = 1;         // warps per ant (k_construct_team when > 1)
     bool exact_only = false; // k_construct_roulette_exact (rows too long to stream)
-    int half_smem = 0;    // pair kernel: bytes per half
     double tau0 = 0.0;
     int64_t max_d = 0;
     int device = 0, num_sms = 0;
@@ -265,31 +263,6 @@ void choose_stream_layout(aco_gpu_ctx* c) {
         c->tabu_words = c->R * c->C + 4;
         return;
     }
-    // Two-ants-per-warp kernel (construct_pair.cuh): bit-exact, but measured
-    // slower at pr2392 (4.98 vs 4.18 ms: 9 warps/SM cannot hide its ~3000-cycle
-    // step), so it is opt-in for experiments.
-    const char* pe = std::getenv("ACO_CONSTRUCT_PAIR");
-    const bool pair_ok = pe && pe[0] == '1';
-    if (pair_ok && c->cfg.selection == ACO_SEL_ROULETTE && c->stream_kind == ACO_STREAM_FP32 &&
-        c->n <= 16 * 160) {
-        // two ants per warp: 16 lanes x C = 4*NV cities per ant
-        static const int pnv[] = {8, 16, 24, 32, 40};
-        for (int nv : pnv)
-            if (16 * 4 * nv >= c->n) {
-                c->NV = nv;
-                break;
-            }
-        c->LA = 16;
-        c->C = 4 * c->NV;
-        c->R = 1;
-        c->MAXR = 1;
-        c->PW = c->NV * 17 * 4;
-        c->tabu_words = 16 * c->C / 32 + 4;
-        const size_t hs = 128 + static_cast<size_t>(c->PW) * 4 + c->tabu_words * 4 +
-                          static_cast<size_t>((c->n + 31) / 32) * 8 + 16 * 4;
-        c->half_smem = static_cast<int>((hs + 127) / 128 * 128);
-        return;
-    }
     c->LA = 32;
     static const int nvs[] = {2, 4, 8, 12, 16, 19, 20};
     c->NV = 0;
@@ -412,7 +385,6 @@ ConstructParams make_cp(aco_gpu_ctx* c) {
     p.iteration = static_cast<uint32_t>(c->iteration);
     p.seed = c->seed;
     p.timing = c->d_timing;
-    p.half_smem = c->half_smem;
     p.topk = c->d_topk;
     p.topk_k = kTopK;
     return p;
@@ -422,30 +394,7 @@ void launch_construct(aco_gpu_ctx* c) {
     ConstructParams p = make_cp(c);
     const size_t smem1 = static_cast<size_t>(c->tabu_words) * sizeof(uint32_t);
     if (c->mloc == 0) return;
-    if (c->cfg.selection == ACO_SEL_ROULETTE && c->LA == 16) {
-        ConstructFn fn = k_construct_roulette_pair<40>;
-        switch (c->NV) {
-        case 8: fn = k_construct_roulette_pair<8>; break;
-        case 16: fn = k_construct_roulette_pair<16>; break;
-        case 24: fn = k_construct_roulette_pair<24>; break;
-        case 32: fn = k_construct_roulette_pair<32>; break;
-        default: break;
-        }
-        const size_t smem = 2 * static_cast<size_t>(c->half_smem);
-        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem));
-        const int pairs = (c->mloc + 1) / 2;
-        const int grid = std::max(1, std::min(pairs, per_sm * c->num_sms));
-        c->construct_grid = grid;
-        c->construct_desc = "k_construct_roulette_pair<" + std::to_string(c->NV) + "> grid=" +
-                            std::to_string(grid) + " per_sm=" + std::to_string(per_sm) +
-                            " smem=" + std::to_string(smem);
-        if (std::getenv("ACO_DEBUG"))
-            std::fprintf(stderr, "construct: %s\n", c->construct_desc.c_str());
-        fn<<<grid, 32, smem, c->stream>>>(p);
-        check_launch(c, "k_construct_roulette_pair");
-    } else if (c->cfg.selection == ACO_SEL_ROULETTE && c->exact_only) {
+    if (c->cfg.selection == ACO_SEL_ROULETTE && c->exact_only) {
         const uint32_t stage_bytes = 16 * 1024;
         const size_t smem = 128 + stage_bytes + smem1 + static_cast<size_t>((c->n + 31) / 32) * sizeof(double) + 8;
         if (smem > 48 * 1024)

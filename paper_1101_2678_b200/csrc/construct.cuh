@@ -37,9 +37,6 @@
 
 #include "philox.cuh"
 
-#ifndef ACO_SCAN32
-#define ACO_SCAN32 0 // lane-sum warp scan in the weight type (fp32) instead of fp64
-#endif
 #ifndef ACO_LDG
 #define ACO_LDG 2 // 1: ld.global.nc.L1::no_allocate; 2: ld.global.nc (L1-allocating)
 #endif
@@ -51,9 +48,6 @@
 #endif
 #ifndef ACO_TIMING
 #define ACO_TIMING 0 // per-phase clock64() accounting into ConstructParams::timing
-#endif
-#ifndef ACO_LANEWALK
-#define ACO_LANEWALK 0 // locate j* inside the crossing chunk with the crossing lane alone
 #endif
 
 namespace acob200 {
@@ -111,7 +105,6 @@ struct ConstructParams {
     uint32_t iteration;
     uint64_t seed;
     unsigned long long* timing; // ACO_TIMING: [8] phase cycle totals
-    int half_smem;              // two-ants-per-warp kernel: bytes of one half's shared area
     const int32_t* topk;        // nn selection: n x topk_k argmax cache (k_row_topk) or null
     int topk_k;
 };
