@@ -530,6 +530,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                 ubatch = philox_uniform(p.seed, p.iteration, kg,
                                         static_cast<uint32_t>(step + lane), 0);
             const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
+            const float u32 = __double2float_rn(u);
             __syncwarp();
             if (!kLDG) {
                 mbar_wait(bar, phase);
@@ -610,7 +611,14 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
             }
             const double Td = static_cast<double>(T);
             const double tdd = u * Td;
-            const AT t = static_cast<AT>(tdd); // compare threshold in AT
+            // Candidate threshold in AT.  Only the candidate search uses it —
+            // certification compares against tdd through A and B — so the
+            // fp32 stream forms it in fp32 from a float copy of u (known at
+            // the top of the step), keeping the double product and its two
+            // conversions off the scan -> ballot chain.
+            AT t;
+            if constexpr (F32) t = __fmul_rn(u32, T);
+            else t = static_cast<AT>(tdd);
             // certification thresholds (T, u only): |t_ref - t| <= Mt
             const double Thi = Td * (1.0 + 0x1.0p-16) + abs_q;
             const double Mt = (e_rel + 4.0 * ulp_at) * (u * Thi) + abs_q; // + rounding of t to AT
