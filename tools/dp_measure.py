@@ -1,3 +1,5 @@
+"""Data-parallel selection (paper Fig. 1, select_next_data_parallel): device
+construction time vs the reference CPU Engine at d198 / pr1002 (pr2392 GPU only)."""
 import sys, time, json, os
 sys.path.insert(0, '.'); sys.path.insert(0, 'oracle')
 from paper_1101_2678_b200 import aco
