@@ -61,6 +61,53 @@ extern "C" int aco_probe_read_bw_mode(int device, size_t bytes, int reps, int it
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
+// red.global.add.f64 throughput at pseudo-random addresses over a buffer of
+// `bytes` (the deposit's access pattern: no locality, no contention) — the
+// atomic roofline of k_deposit_atomic (46 MB: L2-resident like pr2392's tau;
+// 800 MB: HBM-backed like 10k's).
+__global__ void k_red(double* __restrict__ buf, size_t ncells, size_t nops, unsigned seed) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < nops;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        unsigned long long h = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+        h ^= h >> 31;
+        h *= 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 29;
+        atomicAdd(buf + (h % ncells), 1e-9);
+    }
+}
+
+extern "C" int aco_probe_red(int device, size_t bytes, size_t nops, int iters, double* gops,
+                             double* ms_out) {
+    if (cudaSetDevice(device) != cudaSuccess) return 1;
+    double* buf = nullptr;
+    if (cudaMalloc(&buf, bytes) != cudaSuccess) return 2;
+    cudaMemset(buf, 0, bytes);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const size_t ncells = bytes / sizeof(double);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    k_red<<<sms * 8, 256>>>(buf, ncells, nops, 1u);
+    cudaDeviceSynchronize();
+    double best = 1e30;
+    for (int it = 0; it < iters; ++it) {
+        cudaEventRecord(a);
+        k_red<<<sms * 8, 256>>>(buf, ncells, nops, 7u + it);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+    }
+    *ms_out = best;
+    *gops = static_cast<double>(nops) / (best * 1e-3) / 1e9;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(buf);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
 extern "C" int aco_probe_read_bw(int device, size_t bytes, int reps, int iters, double* gbps,
                                  double* ms_out) {
     return aco_probe_read_bw_mode(device, bytes, reps, iters, 0, gbps, ms_out);
