@@ -173,3 +173,27 @@ def test_oracle_degenerate_branches(oracle, reference):
     t2, l2 = reference.construct(d, ch, 2, 0, 0, n)
     assert np.array_equal(t1, t2)
     assert st[2] > 0  # the zero-total branch fired
+
+
+def test_philox_uniform_ks(oracle):
+    """Draw 0 of consecutive steps is uniform on [0, 1) (KS)."""
+    from scipy.stats import kstest
+
+    u = np.array([oracle.uniform_at(1, 0, 0, s, 0) for s in range(20000)])
+    assert u.min() >= 0.0 and u.max() < 1.0
+    assert kstest(u, "uniform").pvalue > 1e-4
+    v = np.array([oracle.uniform_at(1, 0, 1, s, 0) for s in range(20000)])
+    assert np.corrcoef(u, v)[0, 1] < 0.05  # ant streams are separate
+
+
+def test_data_parallel_theta_invariance(oracle, reference):
+    """The reference's tiled data-parallel selection does not depend on the
+    tile size theta, and equals the oracle's (untiled)."""
+    n = 150
+    xs, ys = synth_coords(n)
+    d = oracle.build_dist(xs, ys)
+    ch = oracle.choice(d, np.full((n, n), oracle.tau0(d, n)))
+    base, _, _ = oracle.construct(d, ch, 3, 0, 0, 40, selection=2)
+    for theta in (1, 7, 32, 64, 150, 1000):
+        t, _ = reference.construct(d, ch, 3, 0, 0, 40, selection=2, theta=theta)
+        assert np.array_equal(t, base), theta
