@@ -414,9 +414,12 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": int(d2h),
-                "note": "aco_gpu_iterate with host tours/lengths buffers, host wall clock; the "
-                        "instance (n*n int32 dist + eta^beta table) is copied H2D once at "
-                        f"Engine creation ({create_ms:.1f} ms), colony state stays resident"},
+                "note": "aco_gpu_iterate with pinned host tours/lengths buffers, host wall clock; "
+                        "the construction kernel streams every tour into the (device-mapped) "
+                        "pinned buffer 128 B at a time while it is built, lengths are copied "
+                        "after; the instance (n*n int32 dist + eta^beta table) is copied H2D "
+                        f"once at Engine creation ({create_ms:.1f} ms), colony state stays "
+                        "resident"},
         "gpu_launches": launches,
         "clocks": clocks,
     }

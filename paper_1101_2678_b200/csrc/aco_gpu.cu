@@ -92,6 +92,7 @@ struct aco_gpu_ctx {
     int LA = 32;          // lanes sharing a streamed row
     int team = 1;         // warps per ant (k_construct_team when > 1)
     bool exact_only = false; // k_construct_roulette_exact (rows too long to stream)
+    int32_t* host_tours = nullptr; // this construction's streamed host tour buffer (device view)
     double tau0 = 0.0;
     int64_t max_d = 0;
     int device = 0, num_sms = 0;
@@ -190,20 +191,25 @@ __global__ void k_fill(double* p, size_t count, double v) {
 // ---- construction kernel dispatch ------------------------------------------
 using ConstructFn = void (*)(ConstructParams);
 
-template <typename WT>
-ConstructFn pick_roulette(int NV, int MAXR) {
+template <typename WT, bool ST>
+ConstructFn pick_roulette_s(int NV, int MAXR) {
     if (MAXR == 1) {
         switch (NV) {
-        case 2: return k_construct_roulette<WT, 2, 1>;
-        case 4: return k_construct_roulette<WT, 4, 1>;
-        case 8: return k_construct_roulette<WT, 8, 1>;
-        case 12: return k_construct_roulette<WT, 12, 1>;
-        case 16: return k_construct_roulette<WT, 16, 1>;
-        case 19: return k_construct_roulette<WT, 19, 1>;
-        default: return k_construct_roulette<WT, 20, 1>;
+        case 2: return k_construct_roulette<WT, 2, 1, ST>;
+        case 4: return k_construct_roulette<WT, 4, 1, ST>;
+        case 8: return k_construct_roulette<WT, 8, 1, ST>;
+        case 12: return k_construct_roulette<WT, 12, 1, ST>;
+        case 16: return k_construct_roulette<WT, 16, 1, ST>;
+        case 19: return k_construct_roulette<WT, 19, 1, ST>;
+        default: return k_construct_roulette<WT, 20, 1, ST>;
         }
     }
-    return k_construct_roulette<WT, 20, 8>;
+    return k_construct_roulette<WT, 20, 8, ST>;
+}
+// stream = true: the variant that also streams tours into mapped host memory
+template <typename WT>
+ConstructFn pick_roulette(int NV, int MAXR, bool stream = false) {
+    return stream ? pick_roulette_s<WT, true>(NV, MAXR) : pick_roulette_s<WT, false>(NV, MAXR);
 }
 
 template <int K>
@@ -387,6 +393,7 @@ ConstructParams make_cp(aco_gpu_ctx* c) {
     p.timing = c->d_timing;
     p.topk = c->d_topk;
     p.topk_k = kTopK;
+    p.host_tours = c->host_tours;
     return p;
 }
 
@@ -425,8 +432,9 @@ void launch_construct(aco_gpu_ctx* c) {
         fn<<<grid, 32 * c->team, smem, c->stream>>>(p);
         check_launch(c, "k_construct_team");
     } else if (c->cfg.selection == ACO_SEL_ROULETTE) {
-        ConstructFn fn = c->stream_kind == ACO_STREAM_FP64 ? pick_roulette<double>(c->NV, c->MAXR)
-                                                           : pick_roulette<float>(c->NV, c->MAXR);
+        const bool st = c->host_tours != nullptr;
+        ConstructFn fn = c->stream_kind == ACO_STREAM_FP64 ? pick_roulette<double>(c->NV, c->MAXR, st)
+                                                           : pick_roulette<float>(c->NV, c->MAXR, st);
         const size_t wsz = c->stream_kind == ACO_STREAM_FP64 ? sizeof(double) : sizeof(float);
         const int ng = (c->NV + 3) / 4;
         const size_t smem = 128 + static_cast<size_t>(c->PW) * wsz + smem1 +
@@ -971,7 +979,21 @@ aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* to
         aco_gpu_iter_record tmp{};
         aco_gpu_iter_record* r = rec ? rec : &tmp;
         fill_common(c, r);
+        // The one-warp-per-ant roulette streams each tour into a pinned,
+        // device-mapped tours_out while it is built (TourStream); otherwise
+        // the tours are copied after the construction.
+        c->host_tours = nullptr;
+        if (tours_out && c->cfg.selection == ACO_SEL_ROULETTE && !c->exact_only && c->team == 1 &&
+            c->mloc > 0) {
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, tours_out) == cudaSuccess &&
+                at.type == cudaMemoryTypeHost && at.devicePointer)
+                c->host_tours = static_cast<int32_t*>(at.devicePointer);
+            cudaGetLastError(); // pageable memory: not an error, just no mapping
+        }
+        const bool streamed = c->host_tours != nullptr;
         do_construct(c);
+        c->host_tours = nullptr;
         // sharded: statistics and best tour reduced on the device, in stream
         // order before the update (no host round trip inside the iteration)
         if (c->sharded && !c->external) enqueue_shard_stats(c);
@@ -980,7 +1002,7 @@ aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* to
         // only reads them), and join before returning
         if (tours_out || lengths_out) {
             CK(cudaStreamWaitEvent(c->copy_stream, c->ev[2], 0));
-            if (tours_out)
+            if (tours_out && !streamed)
                 CK(cudaMemcpyAsync(tours_out, c->d_tours, sizeof(int32_t) * c->mloc * (c->n + 1),
                                    cudaMemcpyDeviceToHost, c->copy_stream));
             if (lengths_out)

@@ -107,6 +107,30 @@ struct ConstructParams {
     unsigned long long* timing; // ACO_TIMING: [8] phase cycle totals
     const int32_t* topk;        // nn selection: n x topk_k argmax cache (k_row_topk) or null
     int topk_k;
+    int32_t* host_tours;        // device view of the caller's pinned tours_out (or null):
+                                // the roulette kernel streams each tour there as it grows
+};
+
+// Streams a growing tour to mapped (pinned) host memory 32 entries at a time:
+// lane l holds entry 32c + l of the current 32-entry chunk c; a full chunk
+// leaves as one coalesced 128-byte store over PCIe while construction goes
+// on, so the host copy costs no separate device-to-host transfer.
+// (The row address is recomputed from the kernel parameter at each flush so
+// the hot loop carries one extra register, not a pointer.)
+struct TourStream {
+    int held;
+    __device__ __forceinline__ void put(const ConstructParams& p, int kl, int idx, int city, int lane) {
+        if (!p.host_tours) return;
+        if (lane == (idx & 31)) held = city;
+        if ((idx & 31) == 31)
+            p.host_tours[static_cast<size_t>(kl) * (p.n + 1) + (idx & ~31) + lane] = held;
+    }
+    __device__ __forceinline__ void flush(const ConstructParams& p, int kl, int last_idx, int lane) {
+        if (!p.host_tours) return;
+        const int base = last_idx & ~31;
+        if ((last_idx & 31) != 31 && base + lane <= last_idx)
+            p.host_tours[static_cast<size_t>(kl) * (p.n + 1) + base + lane] = held;
+    }
 };
 
 __device__ __forceinline__ bool tabu_test(const uint32_t* tabu, int j) {
@@ -454,7 +478,7 @@ __device__ __noinline__ int certify_fp64(const WT* buf, const uint32_t* tabu, in
 // fp32 adds on any prefix path are counted in the bound, ~24 * 2^-24), fp64
 // for the fp64 stream.  Only the final two certification compares are fp64.
 // NV = 128-bit vectors per lane per round, C = NV*V, MAXR = max rounds.
-template <typename WT, int NV, int MAXR>
+template <typename WT, int NV, int MAXR, bool STREAM = false>
 __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(ConstructParams p) {
     using VT = typename VecOf<WT>::T;
     using AT = WT; // accumulation type
@@ -506,6 +530,8 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
             tabu[start >> 5] |= 1u << (start & 31);
             tour[0] = start;
         }
+        TourStream hs{0}; // STREAM: the caller's pinned tours_out is mapped
+        if constexpr (STREAM) hs.put(p, kl, 0, start, lane);
         int cur = start;
         unsigned long long fb = 0;
         bool prefetched = false; // row of `cur` already requested by the previous step
@@ -841,6 +867,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                 tabu[next >> 5] |= 1u << (next & 31);
                 tour[step] = next;
             }
+            if constexpr (STREAM) hs.put(p, kl, step, next, lane);
             cur = next;
             TICK(5);
         }
@@ -852,6 +879,10 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
         if (lane == 0) {
             tour[n] = start;
             if (fb) atomicAdd(p.fallbacks, fb);
+        }
+        if constexpr (STREAM) {
+            hs.put(p, kl, n, start, lane);
+            hs.flush(p, kl, n, lane);
         }
         __syncwarp();
     }

@@ -392,3 +392,27 @@ def test_roulette_beyond_streamed_layout_limit(aco, oracle):
         t_ref, l_ref, _ = oracle.construct(prob.dist, oracle.choice(prob.dist, tau), 1, 0, 0, m)
         assert np.array_equal(t, t_ref)
         assert np.array_equal(l, l_ref)
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_iterate_host_tour_buffers(aco, pinned):
+    """aco_gpu_iterate with caller buffers: pinned (device-mapped: the
+    construction kernel streams the tours into it) and pageable (copied after
+    the construction) both return exactly the engine's tours and lengths."""
+    import torch
+
+    n = 1002
+    prob, eng = make(aco, n, deposit=0)
+    with eng:
+        if pinned:
+            tb = torch.empty((n, n + 1), dtype=torch.int32, pin_memory=True).numpy()
+            lb = torch.empty(n, dtype=torch.int64, pin_memory=True).numpy()
+        else:
+            tb = np.empty((n, n + 1), np.int32)
+            lb = np.empty(n, np.int64)
+        for _ in range(2):
+            tb[:] = -7
+            eng.run_iteration(tours_out=tb, lengths_out=lb)
+            t, l = eng.ants()
+            assert np.array_equal(tb, t)
+            assert np.array_equal(lb, l)
