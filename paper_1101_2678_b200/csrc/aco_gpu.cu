@@ -449,7 +449,8 @@ void launch_construct(aco_gpu_ctx* c) {
                             (c->stream_kind == ACO_STREAM_FP64 ? "double," : "float,") +
                             std::to_string(c->NV) + "," + std::to_string(c->MAXR) + "> grid=" +
                             std::to_string(grid) + " per_sm=" + std::to_string(per_sm) +
-                            " smem=" + std::to_string(smem) + " row=" + std::to_string(c->PW);
+                            " smem=" + std::to_string(smem) + " row=" + std::to_string(c->PW) +
+                            (st ? " streams_tours_to_host" : "");
         if (std::getenv("ACO_DEBUG"))
             std::fprintf(stderr, "construct: %s\n", c->construct_desc.c_str());
         fn<<<grid, 32, smem, c->stream>>>(p);

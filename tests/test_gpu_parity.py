@@ -413,6 +413,7 @@ def test_iterate_host_tour_buffers(aco, pinned):
         for _ in range(2):
             tb[:] = -7
             eng.run_iteration(tours_out=tb, lengths_out=lb)
+            assert ("streams_tours_to_host" in eng.describe()) == pinned
             t, l = eng.ants()
             assert np.array_equal(tb, t)
             assert np.array_equal(lb, l)
