@@ -464,7 +464,10 @@ void launch_construct(aco_gpu_ctx* c) {
         k_construct_nn<<<grid, 32, smem1, c->stream>>>(p);
         check_launch(c, "k_construct_nn");
     } else {
-        const size_t smem4 = smem1 * 4;
+        const size_t smem4 = smem1 * 4 + 4 * 1024 * sizeof(int);
+        if (smem4 > 48 * 1024)
+            CK(cudaFuncSetAttribute(k_construct_data_parallel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4));
         const int grid = std::max(1, (c->mloc + 3) / 4);
         c->construct_grid = grid;
         c->construct_desc = "k_construct_data_parallel grid=" + std::to_string(grid);

@@ -1185,9 +1185,10 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
 // the unvisited cities (tile reduction order does not change it), and a
 // non-positive best falls back to the lowest unvisited city.
 __global__ void __launch_bounds__(128) k_construct_data_parallel(ConstructParams p) {
-    extern __shared__ uint32_t smem_tabu[];
+    extern __shared__ uint32_t smem_tabu[]; // [4][tabu_words] tabu, then [4][1024] lists
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint32_t* tabu = smem_tabu + wib * p.tabu_words;
+    int* list = reinterpret_cast<int*>(smem_tabu + 4 * p.tabu_words) + wib * 1024;
     const int n = p.n;
     for (int kl = blockIdx.x * 4 + wib; kl < p.mloc; kl += gridDim.x * 4) {
         const uint32_t kg = static_cast<uint32_t>(p.ant_begin + kl);
@@ -1205,12 +1206,37 @@ __global__ void __launch_bounds__(128) k_construct_data_parallel(ConstructParams
             const double* __restrict__ row = p.w64 + static_cast<size_t>(cur) * p.P64;
             double bs = 0.0;
             int bj = -1;
-            for (int j = lane; j < n; j += 32) {
-                if (tabu_test(tabu, j)) continue;
-                const double u = philox_uniform(p.seed, p.iteration, kg,
-                                                static_cast<uint32_t>(step), static_cast<uint32_t>(j));
-                const double s = row[j] * u;
-                if (bj < 0 || s > bs) { bs = s; bj = j; }
+            // Only unvisited cities draw and score: 1024 cities (32 tabu
+            // words) at a time, their unvisited indices are compacted in
+            // ascending order into the warp's list (popc + warp scan), then
+            // the lanes take list entries round-robin — every lane still
+            // meets its cities in ascending order, so "first max per lane,
+            // then lowest index among equal maxima" is unchanged.
+            for (int w0 = 0; w0 < p.tabu_words; w0 += 32) {
+                const int wd = w0 + lane;
+                uint32_t ub = wd < p.tabu_words ? ~tabu[wd] : 0u;
+                const int cnt = __popc(ub);
+                int incl = cnt;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int y = __shfl_up_sync(kFull, incl, off);
+                    if (lane >= off) incl += y;
+                }
+                const int total = __shfl_sync(kFull, incl, 31);
+                int pos = incl - cnt;
+                while (ub) {
+                    list[pos++] = wd * 32 + __ffs(ub) - 1;
+                    ub &= ub - 1;
+                }
+                __syncwarp();
+                for (int r = lane; r < total; r += 32) {
+                    const int j = list[r];
+                    const double u = philox_uniform(p.seed, p.iteration, kg,
+                                                    static_cast<uint32_t>(step), static_cast<uint32_t>(j));
+                    const double s = row[j] * u;
+                    if (bj < 0 || s > bs) { bs = s; bj = j; }
+                }
+                __syncwarp();
             }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
