@@ -341,7 +341,7 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
     rp.alpha = c->cfg.alpha;
     rp.keep = 1.0 - c->cfg.rho; // pheromone.hpp:179
     const size_t smem = static_cast<size_t>(c->P64) * sizeof(double);
-    const size_t wsmem = smem + 48 * sizeof(double);
+    const size_t wsmem = smem + 64 * sizeof(double);
     if (mode == MODE_GATHER && wsmem <= 32 * 1024) { // one warp per row
         int per_sm = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_gather_warp, 32, wsmem));

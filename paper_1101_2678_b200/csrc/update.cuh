@@ -394,10 +394,15 @@ __global__ void __launch_bounds__(256, 3) k_rows(RowParams p) {
 // is the same sequential fold from 0.0 as gather_cell (pheromone.hpp:133-148).
 // (A __match_any_sync grouping was 9% slower.)  The
 // epilogue (tau update, choice, scaled fp32 stream) is k_rows' own, per warp.
+struct __align__(16) StageEntry {
+    int col;
+    int pad;
+    double w;
+};
 __global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
-    extern __shared__ double wsm[]; // rowbuf[P64] + stage[32] (+ 32 staged columns)
+    extern __shared__ double wsm[]; // rowbuf[P64] + stage[32] 16-byte entries
     double* rowbuf = wsm;
-    double* stage = wsm + p.P64;
+    StageEntry* st = reinterpret_cast<StageEntry*>(wsm + p.P64);
     const int lane = threadIdx.x & 31;
     const int n = p.n;
     constexpr int AHEAD = 8;
@@ -426,24 +431,22 @@ __global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
                 }
 #pragma unroll
                 for (int u = 0; u < AHEAD; ++u) {
-                    // stage (column, weight) of the chunk; each lane folds the
-                    // entries of its own column in lane (= ant) order
-                    int* scol = reinterpret_cast<int*>(stage + 32);
+                    // stage (column, weight) of the chunk as 16-byte entries;
+                    // each lane folds the entries of its own column in lane
+                    // (= ant) order — one LDS.128, one compare and one
+                    // predicated DADD per entry — and every lane of a column
+                    // stores the same folded value
                     const int cu = col[u];
-                    stage[lane] = w[u];
-                    scol[lane] = cu;
+                    st[lane] = StageEntry{cu, 0, w[u]};
                     __syncwarp();
                     double acc = cu >= 0 ? rowbuf[cu] : 0.0;
-                    int first = 32;
 #pragma unroll
                     for (int q = 0; q < 32; ++q) {
-                        const bool mq = scol[q] == cu;
-                        const double v = stage[q];
-                        acc = mq ? __dadd_rn(acc, v) : acc;
-                        first = (mq && first == 32) ? q : first;
+                        const StageEntry e = st[q];
+                        if (e.col == cu) acc = __dadd_rn(acc, e.w);
                     }
                     __syncwarp();
-                    if (cu >= 0 && first == lane) rowbuf[cu] = acc;
+                    if (cu >= 0) rowbuf[cu] = acc;
                     __syncwarp();
                 }
             }
