@@ -515,6 +515,8 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
          (F32 ? 2.0 * 0x1.0p-24 : 0.0) + (double)(n + 8) * 0x1.0p-53) * (1.0 + 0x1.0p-16);
     const double abs_q = F32 ? (double)n * 0x1.0p-149 : 0.0;
     const double lo_f = 1.0 - e_rel;
+    const float lo32 = __double2float_rd(lo_f); // <= lo_f
+    const float e32 = __double2float_ru(e_rel); // >= e_rel
 
     if (lane == 0) mbar_init(bar, 1);
     __syncwarp();
@@ -727,11 +729,16 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                             if (x0 > AT(0) && p0 > t) { E = 0; Pj32 = p0; Pp32 = kb; }
                             const unsigned qb = __ballot_sync(kFull, lane < 4 && E >= 0);
                             const bool mine = qb != 0u && lane == __ffs(qb) - 1;
-                            const double Pj = static_cast<double>(Pj32);
-                            const double Pprev = static_cast<double>(Pp32);
+                            // The certification in fp32 with directed rounding
+                            // (implies the fp64 form): Pj*lo_f >= rd(Pj*lo32) >
+                            // A32 >= A and Pprev + e*Pj <= ru(Pprev + ru(e32*Pj))
+                            // < B32 <= B, with lo32 <= lo_f, e32 >= e_rel.
+                            const float A32 = __double2float_ru(A);
+                            const float B32 = __double2float_rd(B);
                             const int Jc = c0 + E;
                             J = mine ? Jc : -1;
-                            cert = mine && (Pj * lo_f > A) && (Pprev + e_rel * Pj < B) && Jc < n;
+                            cert = mine && (__fmul_rd(Pj32, lo32) > A32) &&
+                                   (__fadd_ru(Pp32, __fmul_ru(e32, Pj32)) < B32) && Jc < n;
                         }
                     }
                 } else {
