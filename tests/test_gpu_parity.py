@@ -417,3 +417,41 @@ def test_iterate_host_tour_buffers(aco, pinned):
             t, l = eng.ants()
             assert np.array_equal(tb, t)
             assert np.array_equal(lb, l)
+
+
+@pytest.mark.parametrize("alpha,beta,rho", [(0.0, 2.0, 0.5), (1.0, 1.0, 0.1), (1.0, 3.0, 0.9),
+                                            (1.0, 2.5, 0.25)])
+def test_parameter_variants_bit_exact(aco, oracle, alpha, beta, rho):
+    """alpha in {0, 1} (pow exact) with other beta (the host-libm eta^beta
+    table) and rho: tours and the gather tau stay bit-exact."""
+    n = 300
+    prob, eng = make(aco, n, deposit=1, alpha=alpha, beta=beta, rho=rho)
+    with eng:
+        tau = np.full((n, n), eng.tau0)
+        for it in range(3):
+            ch = oracle.choice(prob.dist, tau, alpha=alpha, beta=beta)
+            assert np.array_equal(eng.choice(), ch)
+            eng.run_iteration()
+            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, 0, n)
+            assert np.array_equal(eng.ants()[0], t_ref), f"iteration {it}"
+            tau = oracle.update(tau, t_ref, l_ref, rho, 1)
+            assert np.array_equal(eng.pheromone(), tau)
+
+
+@pytest.mark.parametrize("ewt", ["ceil_2d", "att"])
+def test_edge_weight_types_bit_exact(aco, oracle, ewt):
+    """CEIL_2D and ATT distances (tsplib.hpp:190-210) through the whole
+    iteration: tours and the gather tau bit-exact."""
+    n = 200
+    base = aco.synthetic_instance(n)
+    spec = aco.InstanceSpec(f"{ewt}{n}", n, getattr(aco.EdgeWeightType, ewt), base.xs, base.ys)
+    prob, eng = make(aco, n, deposit=1, spec=spec)
+    with eng:
+        tau = np.full((n, n), eng.tau0)
+        for it in range(2):
+            ch = oracle.choice(prob.dist, tau)
+            eng.run_iteration()
+            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, 0, n)
+            assert np.array_equal(eng.ants()[0], t_ref)
+            tau = oracle.update(tau, t_ref, l_ref, 0.5, 1)
+            assert np.array_equal(eng.pheromone(), tau)
