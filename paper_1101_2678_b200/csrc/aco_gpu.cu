@@ -117,6 +117,8 @@ struct aco_gpu_ctx {
     int32_t* d_scale = nullptr;
     int32_t* d_nn = nullptr;
     double* d_choice_nn = nullptr; // n x nn
+    float* d_choice_nn32 = nullptr; // n x nn, row-scaled fp32 (nn <= 32)
+    int32_t* d_nn_scale = nullptr;  // n
     int32_t* d_topk = nullptr;     // n x kTopK argmax cache (nn selection)
     long long last_fb[2] = {0, 0}; // last construction: exact/full-scan, argmax fallbacks
     int32_t* d_tours = nullptr;
@@ -328,6 +330,8 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
     rp.inv = c->d_inv;
     rp.nn_lists = c->d_nn;
     rp.choice_nn = c->d_choice_nn;
+    rp.choice_nn32 = c->d_choice_nn32;
+    rp.nn_scale = c->d_nn_scale;
     rp.nn = c->cfg.nn;
     rp.n = c->n;
     rp.P64 = c->P64;
@@ -375,6 +379,7 @@ ConstructParams make_cp(aco_gpu_ctx* c) {
     p.w64 = c->d_choice;
     p.nn_lists = c->d_nn;
     p.choice_nn = c->d_choice_nn;
+    p.choice_nn32 = c->d_choice_nn32;
     p.tours = c->d_tours;
     p.fallbacks = c->d_fb;
     p.argmax_fallbacks = c->d_fb + 1;
@@ -797,6 +802,10 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
             CK(cudaMemcpy(c->d_nn, nn_host.data(), nn_host.size() * sizeof(int32_t),
                           cudaMemcpyHostToDevice));
             CK(cudaMalloc(&c->d_choice_nn, nn_host.size() * sizeof(double)));
+            if (c->cfg.nn <= 32) {
+                CK(cudaMalloc(&c->d_choice_nn32, nn_host.size() * sizeof(float)));
+                CK(cudaMalloc(&c->d_nn_scale, n * sizeof(int32_t)));
+            }
             const char* tke = std::getenv("ACO_NN_TOPK"); // "0" disables the argmax cache
             if (!(tke && tke[0] == '0'))
                 CK(cudaMalloc(&c->d_topk, static_cast<size_t>(n) * kTopK * sizeof(int32_t)));
@@ -877,7 +886,7 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
-    void* bufs[] = {c->d_choice_nn, c->d_topk, c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
+    void* bufs[] = {c->d_choice_nn, c->d_choice_nn32, c->d_nn_scale, c->d_topk, c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
                     c->d_choice_p64, c->d_scale, c->d_nn, c->d_tours, c->d_len, c->d_inv,
                     c->d_succ, c->d_pred, c->d_delta, c->d_stats, c->d_best, c->d_fb, c->d_tourbuf};
     for (void* b : bufs)

@@ -94,6 +94,7 @@ struct ConstructParams {
     const double* w64;       // natural fp64 choice, row pitch P64 (exact walk, nn)
     const int32_t* nn_lists; // n x nn (nn selection)
     const double* choice_nn; // n x nn weights of the nn lists (nn selection)
+    const float* choice_nn32; // n x nn, row-scaled fp32 copy (nn <= 32) or null
     int32_t* tours;          // mloc x (n+1)
     unsigned long long* fallbacks;
     unsigned long long* argmax_fallbacks;
@@ -987,7 +988,56 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
             const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
             int next = -1;
             bool exhausted = false; // every list member visited: argmax fallback
-            if (nn <= 32) {
+            if (nn <= 32 && p.choice_nn32) {
+                // Fast path on the row-scaled fp32 copy of the list weights
+                // (k_rows: the list maximum scaled into [2^100, 2^101) by an
+                // exact power of two, so scaled and unscaled comparisons
+                // agree): one fp32 warp scan, then the crossing J is
+                // CERTIFIED against the reference's fp64 sequential sums —
+                // |P_q - X_q| <= e*X_q + nn*2^-150 with e covering the fp32
+                // quantisation (1 ulp), the 5 scan levels and the
+                // reference's own nn sequential fp64 adds; thresholds are
+                // rounded outward so the fp32 compares imply the exact ones.
+                // T == 0 (possible through fp32 underflow) and uncertain
+                // steps take the exact fp64 fold below.
+                const int q = lane;
+                int j = -1;
+                float w = 0.f;
+                bool un = false;
+                if (q < nn) {
+                    j = nb[q];
+                    const float wq0 = p.choice_nn32[static_cast<size_t>(cur) * nn + q];
+                    un = !tabu_test(tabu, j);
+                    w = un ? wq0 : 0.f;
+                }
+                const unsigned unb = __ballot_sync(kFull, un);
+                if (!unb) {
+                    exhausted = true;
+                } else {
+                    const float P = warp_inclusive_scan(w);
+                    const float T = __shfl_sync(kFull, P, 31);
+                    const float Eu = __shfl_up_sync(kFull, P, 1); // every lane shuffles
+                    const float E = lane == 0 ? 0.f : Eu;
+                    const float t32 = __fmul_rn(__double2float_rn(u), T);
+                    const unsigned cr = __ballot_sync(kFull, q < nn && w > 0.f && P > t32 && T > 0.f);
+                    if (cr) {
+                        const int J = __ffs(cr) - 1;
+                        const float PJ = __shfl_sync(kFull, P, J);
+                        const float EJ = __shfl_sync(kFull, E, J);
+                        const int Jc = __shfl_sync(kFull, j, J);
+                        const double e = (12.0 * 0x1.0p-24 + (double)(nn + 8) * 0x1.0p-53) * (1.0 + 0x1.0p-16);
+                        const double absq = (double)nn * 0x1.0p-149;
+                        const double Td = static_cast<double>(T);
+                        const double tdd = u * Td;
+                        const double Mt = (e + 4.0 * 0x1.0p-24) * (u * (Td * (1.0 + 0x1.0p-16) + absq)) + absq;
+                        const float A32 = __double2float_ru(tdd + Mt + 2.0 * absq);
+                        const float B32 = __double2float_rd(tdd - Mt - 2.0 * absq);
+                        const float lo32 = __double2float_rd(1.0 - e);
+                        const float e32 = __double2float_ru(e);
+                        if (__fmul_rd(PJ, lo32) > A32 && __fadd_ru(EJ, __fmul_ru(e32, PJ)) < B32) next = Jc;
+                    }
+                }
+            } else if (nn <= 32) {
                 // Fast path: one fp64 warp scan instead of the sequential
                 // fold, then CERTIFY the crossing against the reference's
                 // sequential sums (as in k_construct_roulette): every scan

@@ -197,6 +197,8 @@ struct RowParams {
     const double* inv;       // [shard][S]
     const int32_t* nn_lists; // n x nn (nn selection) or null
     double* choice_nn;       // n x nn: choice64[i][nn_lists[i][q]] (nn selection)
+    float* choice_nn32;      // n x nn: the same scaled by 2^nn_scale[i] (row max -> [2^100, 2^101)), fp32
+    int32_t* nn_scale;       // n
     int nn;
     int n, P64, PW, C, V, LA;
     int shards, S, m;        // ants: shard g holds global ants [g*S, min(m,(g+1)*S))
@@ -235,6 +237,29 @@ __device__ __forceinline__ void write_stream_row(OT* __restrict__ crow, const do
             }
             reinterpret_cast<double2*>(crow)[s] = o;
         }
+    }
+}
+
+// Row i's nn list weights (one warp, lanes = members; nn <= 32 for the
+// fp32 copy): fp64 for the exact paths, and an fp32 copy scaled by the
+// exact power of two that puts the list maximum in [2^100, 2^101) for the
+// nn fast path's fp32 scan (a scaled weight below 2^-126 only loses
+// absolute precision, <= 2^-150 each, which the certification counts).
+__device__ __forceinline__ void write_nn_row(const RowParams& p, const double* src, int i, int lane) {
+    const size_t base = static_cast<size_t>(i) * p.nn;
+    double w = 0.0;
+    if (lane < p.nn) {
+        w = src[p.nn_lists[base + lane]];
+        p.choice_nn[base + lane] = w;
+    }
+    for (int q = lane + 32; q < p.nn; q += 32) p.choice_nn[base + q] = src[p.nn_lists[base + q]];
+    if (p.choice_nn32 && p.nn <= 32) {
+        double mx = w;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, off));
+        const int sc = mx > 0.0 ? 100 - ilogb(mx) : 0;
+        if (lane < p.nn) p.choice_nn32[base + lane] = __double2float_rn(scalbn(w, sc));
+        if (lane == 0) p.nn_scale[i] = sc;
     }
 }
 
@@ -359,11 +384,9 @@ __global__ void __launch_bounds__(256, 3) k_rows(RowParams p) {
             if (lane == 0) s_max[warp] = mx;
         }
         if (need_sync) __syncthreads(); // also orders this block's choice64 stores
-        if (p.choice_nn) { // the nn list's weights, contiguous per row (L2-resident)
+        if (p.choice_nn && warp == 0) { // the nn list's weights, contiguous per row (L2-resident)
             const double* src = use_row ? rowbuf : p.choice64 + static_cast<size_t>(i) * p.P64;
-            for (int q = tid; q < p.nn; q += blockDim.x)
-                p.choice_nn[static_cast<size_t>(i) * p.nn + q] =
-                    src[p.nn_lists[static_cast<size_t>(i) * p.nn + q]];
+            write_nn_row(p, src, i, lane);
         }
         if (p.choice32) {
             double rmx = 0.0;
@@ -488,10 +511,7 @@ __global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, off));
         __syncwarp();
-        if (p.choice_nn)
-            for (int q = lane; q < p.nn; q += 32)
-                p.choice_nn[static_cast<size_t>(i) * p.nn + q] =
-                    rowbuf[p.nn_lists[static_cast<size_t>(i) * p.nn + q]];
+        if (p.choice_nn) write_nn_row(p, rowbuf, i, lane);
         if (p.choice32) {
             const int sc = mx > 0.0 ? 100 - ilogb(mx) : 0;
             if (lane == 0) p.scale_exp[i] = sc;
