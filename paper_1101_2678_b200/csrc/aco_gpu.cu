@@ -347,11 +347,25 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
     const size_t smem = static_cast<size_t>(c->P64) * sizeof(double);
     const size_t wsmem = smem + 64 * sizeof(double);
     if (mode == MODE_GATHER && wsmem <= 32 * 1024) { // one warp per row
+        // Default: fold-only warp kernel (ordered sums -> delta rows) and the
+        // tau/choice epilogue by k_rows<DELTA> at full CTA occupancy (pr2392:
+        // 0.26 -> 0.20 ms); ACO_GATHER_SPLIT=0 keeps the epilogue in the warp
+        // kernel.
+        const bool split = c->d_delta != nullptr;
+        auto fn = split ? k_rows_gather_warp<false> : k_rows_gather_warp<true>;
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_gather_warp, 32, wsmem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, wsmem));
         const int grid = std::max(1, std::min(c->n, per_sm * c->num_sms));
-        k_rows_gather_warp<<<grid, 32, wsmem, c->stream>>>(rp);
+        fn<<<grid, 32, wsmem, c->stream>>>(rp);
         check_launch(c, "k_rows_gather_warp");
+        if (split) {
+            const size_t dsmem = (rp.choice32 || rp.choice_perm64) ? smem : 0;
+            if (dsmem > 48 * 1024)
+                CK(cudaFuncSetAttribute(k_rows<MODE_DELTA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)dsmem));
+            k_rows<MODE_DELTA><<<std::min(c->n, c->num_sms * 8), 256, dsmem, c->stream>>>(rp);
+            check_launch(c, "k_rows");
+        }
         launch_topk(c);
         return;
     }
@@ -823,7 +837,12 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
             CK(cudaMalloc(&c->d_pred, sp * sizeof(int32_t)));
             CK(cudaMemset(c->d_succ, 0, sp * sizeof(int32_t)));
             CK(cudaMemset(c->d_pred, 0, sp * sizeof(int32_t)));
-        } else if (c->sharded) {
+        }
+        const char* gsplit = std::getenv("ACO_GATHER_SPLIT");
+        const bool warp_gather = c->cfg.deposit != ACO_DEP_ACCUMULATE &&
+                                 static_cast<size_t>(c->P64) * sizeof(double) + 64 * sizeof(double) <= 32 * 1024;
+        if ((c->sharded && c->cfg.deposit == ACO_DEP_ACCUMULATE) ||
+            (warp_gather && !(gsplit && gsplit[0] == '0'))) {
             CK(cudaMalloc(&c->d_delta, cells * sizeof(double)));
             CK(cudaMemset(c->d_delta, 0, cells * sizeof(double)));
         }

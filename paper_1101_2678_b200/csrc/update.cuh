@@ -422,6 +422,10 @@ struct __align__(16) StageEntry {
     int pad;
     double w;
 };
+// EPI = false: fold only — the row's ordered sums go to p.delta (row i) and
+// k_rows<MODE_DELTA> applies tau = fl(fl(tau*keep) + delta) (the same two
+// roundings) and the choice epilogue at full CTA occupancy.
+template <bool EPI>
 __global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
     extern __shared__ double wsm[]; // rowbuf[P64] + stage[32] 16-byte entries
     double* rowbuf = wsm;
@@ -473,6 +477,12 @@ __global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
                     __syncwarp();
                 }
             }
+        }
+        if constexpr (!EPI) {
+            double* drow = p.delta + static_cast<size_t>(i) * p.P64;
+            for (int j = lane; j < n; j += 32) drow[j] = rowbuf[j];
+            __syncwarp();
+            continue;
         }
         double mx = 0.0;
         const int32_t* drow = p.dist + static_cast<size_t>(i) * p.P64;
