@@ -422,6 +422,9 @@ struct __align__(16) StageEntry {
     int pad;
     double w;
 };
+#ifndef ACO_GATHER_AHEAD
+#define ACO_GATHER_AHEAD 8 // 16-ant chunks whose contributions are loaded together
+#endif
 // EPI = false: fold only — the row's ordered sums go to p.delta (row i) and
 // k_rows<MODE_DELTA> applies tau = fl(fl(tau*keep) + delta) (the same two
 // roundings) and the choice epilogue at full CTA occupancy.
@@ -432,7 +435,7 @@ __global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
     StageEntry* st = reinterpret_cast<StageEntry*>(wsm + p.P64);
     const int lane = threadIdx.x & 31;
     const int n = p.n;
-    constexpr int AHEAD = 8;
+    constexpr int AHEAD = ACO_GATHER_AHEAD;
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
         double* trow = p.tau + static_cast<size_t>(i) * p.P64;
         for (int j = lane; j < n; j += 32) rowbuf[j] = 0.0;
