@@ -455,3 +455,22 @@ def test_edge_weight_types_bit_exact(aco, oracle, ewt):
             assert np.array_equal(eng.ants()[0], t_ref)
             tau = oracle.update(tau, t_ref, l_ref, 0.5, 1)
             assert np.array_equal(eng.pheromone(), tau)
+
+
+@pytest.mark.parametrize("nn", [33, 48, 64])
+def test_nn_long_lists_bit_exact(aco, oracle, nn):
+    """nn lists longer than a warp (two passes of the exact fold, no fp32
+    fast path): tours and the gather tau bit-exact."""
+    n = 300
+    prob, eng = make(aco, n, selection=1, deposit=1, nn=nn)
+    with eng:
+        nnl = oracle.nn_lists(prob.dist, nn)
+        tau = np.full((n, n), eng.tau0)
+        for it in range(2):
+            ch = oracle.choice(prob.dist, tau)
+            eng.run_iteration()
+            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, 0, n, selection=1,
+                                               nn_lists=nnl)
+            assert np.array_equal(eng.ants()[0], t_ref), f"iteration {it}"
+            tau = oracle.update(tau, t_ref, l_ref, 0.5, 1)
+            assert np.array_equal(eng.pheromone(), tau)
