@@ -978,6 +978,16 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
         int cur = start;
         unsigned long long fb = 0, fb_full = 0;
         double ubatch = 0.0;
+        // fp32 fast path: the current city's list (ids, scaled weights) is
+        // loaded as soon as that city is chosen, one step ahead, so the L2
+        // round trip overlaps the previous step's bookkeeping
+        const bool fast32 = nn <= 32 && p.choice_nn32 != nullptr;
+        int jpre = -1;
+        float wpre = 0.f;
+        if (fast32 && lane < nn) {
+            jpre = p.nn_lists[static_cast<size_t>(start) * nn + lane];
+            wpre = p.choice_nn32[static_cast<size_t>(start) * nn + lane];
+        }
         for (int step = 1; step < n; ++step) {
             const double* __restrict__ row = p.w64 + static_cast<size_t>(cur) * p.P64;
             const int32_t* nb = p.nn_lists + static_cast<size_t>(cur) * nn;
@@ -988,7 +998,7 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
             const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
             int next = -1;
             bool exhausted = false; // every list member visited: argmax fallback
-            if (nn <= 32 && p.choice_nn32) {
+            if (fast32) {
                 // Fast path on the row-scaled fp32 copy of the list weights
                 // (k_rows: the list maximum scaled into [2^100, 2^101) by an
                 // exact power of two, so scaled and unscaled comparisons
@@ -1005,10 +1015,9 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
                 float w = 0.f;
                 bool un = false;
                 if (q < nn) {
-                    j = nb[q];
-                    const float wq0 = p.choice_nn32[static_cast<size_t>(cur) * nn + q];
+                    j = jpre;
                     un = !tabu_test(tabu, j);
-                    w = un ? wq0 : 0.f;
+                    w = un ? wpre : 0.f;
                 }
                 const unsigned unb = __ballot_sync(kFull, un);
                 if (!unb) {
@@ -1159,6 +1168,10 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
                         }
                     }
                     if (next >= 0) {
+                        if (fast32 && lane < nn && step + 1 < n) {
+                            jpre = p.nn_lists[static_cast<size_t>(next) * nn + lane];
+                            wpre = p.choice_nn32[static_cast<size_t>(next) * nn + lane];
+                        }
                         if (lane == 0) {
                             tabu[next >> 5] |= 1u << (next & 31);
                             tour[step] = next;
@@ -1218,6 +1231,10 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
                     if (oj >= 0 && (bj < 0 || ow > bw || (ow == bw && oj < bj))) { bw = ow; bj = oj; }
                 }
                 next = bj;
+            }
+            if (fast32 && lane < nn && step + 1 < n) {
+                jpre = p.nn_lists[static_cast<size_t>(next) * nn + lane];
+                wpre = p.choice_nn32[static_cast<size_t>(next) * nn + lane];
             }
             if (lane == 0) {
                 tabu[next >> 5] |= 1u << (next & 31);
