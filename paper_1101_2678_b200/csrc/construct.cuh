@@ -964,6 +964,14 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
     uint32_t* tabu = smem_tabu;
     const int lane = threadIdx.x & 31;
     const int n = p.n, nn = p.nn;
+    // fp32 fast-path certification constants (outward-rounded): e counts the
+    // fp32 quantisation (1 ulp), 5 scan levels, margins, and the reference's
+    // nn sequential fp64 adds; nn * 2^-149 bounds the subnormal losses
+    const double nn_e = (12.0 * 0x1.0p-24 + (double)(nn + 8) * 0x1.0p-53) * (1.0 + 0x1.0p-16);
+    const float nn_e32 = __double2float_ru(nn_e);
+    const float nn_lo32 = __double2float_rd(1.0 - nn_e);
+    const float nn_ce = __double2float_ru(nn_e + 4.0 * 0x1.0p-24);
+    const float nn_absq = static_cast<float>(nn) * 0x1.0p-149f; // exact: a subnormal multiple
     for (int kl = blockIdx.x; kl < p.mloc; kl += gridDim.x) {
         const uint32_t kg = static_cast<uint32_t>(p.ant_begin + kl);
         int32_t* tour = p.tours + static_cast<size_t>(kl) * (n + 1);
@@ -996,6 +1004,7 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
                 ubatch = philox_uniform(p.seed, p.iteration, kg,
                                         static_cast<uint32_t>(step + lane), 0);
             const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
+            const float u_up = __double2float_ru(u), u_dn = __double2float_rd(u);
             int next = -1;
             bool exhausted = false; // every list member visited: argmax fallback
             if (fast32) {
@@ -1034,16 +1043,15 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
                         const float PJ = __shfl_sync(kFull, P, J);
                         const float EJ = __shfl_sync(kFull, E, J);
                         const int Jc = __shfl_sync(kFull, j, J);
-                        const double e = (12.0 * 0x1.0p-24 + (double)(nn + 8) * 0x1.0p-53) * (1.0 + 0x1.0p-16);
-                        const double absq = (double)nn * 0x1.0p-149;
-                        const double Td = static_cast<double>(T);
-                        const double tdd = u * Td;
-                        const double Mt = (e + 4.0 * 0x1.0p-24) * (u * (Td * (1.0 + 0x1.0p-16) + absq)) + absq;
-                        const float A32 = __double2float_ru(tdd + Mt + 2.0 * absq);
-                        const float B32 = __double2float_rd(tdd - Mt - 2.0 * absq);
-                        const float lo32 = __double2float_rd(1.0 - e);
-                        const float e32 = __double2float_ru(e);
-                        if (__fmul_rd(PJ, lo32) > A32 && __fadd_ru(EJ, __fmul_ru(e32, PJ)) < B32) next = Jc;
+                        // thresholds in fp32, every operation rounded
+                        // outward: A32 >= u*T + Mt + 2*abs, B32 <= u*T - Mt -
+                        // 2*abs, Mt >= (e + 4*2^-24) * u * (T(1+2^-16) + abs)
+                        // + abs (|t_ref - u*T| <= Mt)
+                        const float Thi = __fadd_ru(__fmul_ru(T, 1.0f + 0x1.0p-16f), nn_absq);
+                        const float Mt = __fadd_ru(__fmul_ru(nn_ce, __fmul_ru(u_up, Thi)), nn_absq);
+                        const float A32 = __fadd_ru(__fadd_ru(__fmul_ru(u_up, T), Mt), 2.0f * nn_absq);
+                        const float B32 = __fsub_rd(__fsub_rd(__fmul_rd(u_dn, T), Mt), 2.0f * nn_absq);
+                        if (__fmul_rd(PJ, nn_lo32) > A32 && __fadd_ru(EJ, __fmul_ru(nn_e32, PJ)) < B32) next = Jc;
                     }
                 }
             } else if (nn <= 32) {
