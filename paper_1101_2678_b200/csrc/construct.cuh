@@ -1009,7 +1009,7 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
             bool exhausted = false; // every list member visited: argmax fallback
             if (fast32) {
                 // Fast path on the row-scaled fp32 copy of the list weights
-                // (k_rows: the list maximum scaled into [2^100, 2^101) by an
+                // (k_rows: the list maximum scaled into [2^112, 2^113) by an
                 // exact power of two, so scaled and unscaled comparisons
                 // agree): one fp32 warp scan, then the crossing J is
                 // CERTIFIED against the reference's fp64 sequential sums —

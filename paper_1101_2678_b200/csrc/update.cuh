@@ -197,7 +197,7 @@ struct RowParams {
     const double* inv;       // [shard][S]
     const int32_t* nn_lists; // n x nn (nn selection) or null
     double* choice_nn;       // n x nn: choice64[i][nn_lists[i][q]] (nn selection)
-    float* choice_nn32;      // n x nn: the same scaled by 2^nn_scale[i] (row max -> [2^100, 2^101)), fp32
+    float* choice_nn32;      // n x nn: the same scaled by 2^nn_scale[i] (row max -> [2^kScaleExp, 2^(kScaleExp+1))), fp32
     int32_t* nn_scale;       // n
     int nn;
     int n, P64, PW, C, V, LA;
@@ -240,9 +240,16 @@ __device__ __forceinline__ void write_stream_row(OT* __restrict__ crow, const do
     }
 }
 
+// Exponent the streamed fp32 copies scale each row's maximum to: the max
+// lands in [2^kScaleExp, 2^(kScaleExp+1)), so a sum of up to 2^15 weights
+// stays below FLT_MAX (2^128) while small weights keep as many bits as
+// possible before becoming subnormal (a subnormal weight only costs the
+// certification its absolute 2^-150 term).
+constexpr int kScaleExp = 112;
+
 // Row i's nn list weights (one warp, lanes = members; nn <= 32 for the
 // fp32 copy): fp64 for the exact paths, and an fp32 copy scaled by the
-// exact power of two that puts the list maximum in [2^100, 2^101) for the
+// exact power of two that puts the list maximum in [2^112, 2^113) for the
 // nn fast path's fp32 scan (a scaled weight below 2^-126 only loses
 // absolute precision, <= 2^-150 each, which the certification counts).
 __device__ __forceinline__ void write_nn_row(const RowParams& p, const double* src, int i, int lane) {
@@ -257,7 +264,7 @@ __device__ __forceinline__ void write_nn_row(const RowParams& p, const double* s
         double mx = w;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, off));
-        const int sc = mx > 0.0 ? 100 - ilogb(mx) : 0;
+        const int sc = mx > 0.0 ? kScaleExp - ilogb(mx) : 0;
         if (lane < p.nn) p.choice_nn32[base + lane] = __double2float_rn(scalbn(w, sc));
         if (lane == 0) p.nn_scale[i] = sc;
     }
@@ -391,8 +398,8 @@ __global__ void __launch_bounds__(256, 3) k_rows(RowParams p) {
         if (p.choice32) {
             double rmx = 0.0;
             for (int w = 0; w < (int)(blockDim.x >> 5); ++w) rmx = fmax(rmx, s_max[w]);
-            // Exact power-of-two scale: row max -> [2^100, 2^101).
-            const int sc = rmx > 0.0 ? 100 - ilogb(rmx) : 0;
+            // Exact power-of-two scale: row max -> [2^kScaleExp, 2^(kScaleExp+1)).
+            const int sc = rmx > 0.0 ? kScaleExp - ilogb(rmx) : 0;
             if (tid == 0) p.scale_exp[i] = sc;
             write_stream_row<4>(p.choice32 + static_cast<size_t>(i) * p.PW, rowbuf, n, p.PW, p.C,
                                 p.LA, sc, tid, blockDim.x); // pads 0
@@ -526,7 +533,7 @@ __global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
         __syncwarp();
         if (p.choice_nn) write_nn_row(p, rowbuf, i, lane);
         if (p.choice32) {
-            const int sc = mx > 0.0 ? 100 - ilogb(mx) : 0;
+            const int sc = mx > 0.0 ? kScaleExp - ilogb(mx) : 0;
             if (lane == 0) p.scale_exp[i] = sc;
             write_stream_row<4>(p.choice32 + static_cast<size_t>(i) * p.PW, rowbuf, n, p.PW, p.C,
                                 p.LA, sc, lane, 32);
