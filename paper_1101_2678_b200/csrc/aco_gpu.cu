@@ -98,6 +98,7 @@ struct aco_gpu_ctx {
     int device = 0, num_sms = 0;
     int construct_grid = 0;
     std::string construct_desc;  // kernel + launch shape of the last construction
+    bool fused_tail = false;     // the last construction kernel also formed len/inv(/succ/pred)
     int iteration = 0;
     int64_t best_so_far = std::numeric_limits<int64_t>::max();
     int64_t launches = 0;
@@ -386,6 +387,8 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
     launch_topk(c);
 }
 
+bool gather_mode(const aco_gpu_ctx* c) { return c->cfg.deposit != ACO_DEP_ACCUMULATE; }
+
 ConstructParams make_cp(aco_gpu_ctx* c) {
     ConstructParams p{};
     p.w = c->stream_kind == ACO_STREAM_FP64 ? static_cast<const void*>(c->d_choice_p64)
@@ -413,11 +416,29 @@ ConstructParams make_cp(aco_gpu_ctx* c) {
     p.topk = c->d_topk;
     p.topk_k = kTopK;
     p.host_tours = c->host_tours;
+    p.dist = c->d_dist;
+    p.inv_out = c->d_inv + static_cast<size_t>(c->rank) * c->S;
+    if (gather_mode(c)) {
+        p.succ_out = c->d_succ + static_cast<size_t>(c->rank) * c->n * c->S;
+        p.pred_out = c->d_pred + static_cast<size_t>(c->rank) * c->n * c->S;
+    }
+    p.S = c->S;
     return p;
+}
+
+// the roulette and nn kernels form the tour lengths in their tail
+// (tour_tail); ACO_FUSED_TAIL=0 keeps the separate k_tour_length launch
+bool fused_tail_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("ACO_FUSED_TAIL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 void launch_construct(aco_gpu_ctx* c) {
     ConstructParams p = make_cp(c);
+    c->fused_tail = false;
     const size_t smem1 = static_cast<size_t>(c->tabu_words) * sizeof(uint32_t);
     if (c->mloc == 0) return;
     if (c->cfg.selection == ACO_SEL_ROULETTE && c->exact_only) {
@@ -472,6 +493,10 @@ void launch_construct(aco_gpu_ctx* c) {
                             (st ? " streams_tours_to_host" : "");
         if (std::getenv("ACO_DEBUG"))
             std::fprintf(stderr, "construct: %s\n", c->construct_desc.c_str());
+        if (fused_tail_enabled()) {
+            p.len_out = c->d_len;
+            c->fused_tail = true;
+        }
         fn<<<grid, 32, smem, c->stream>>>(p);
         check_launch(c, "k_construct_roulette");
     } else if (c->cfg.selection == ACO_SEL_NN) {
@@ -480,6 +505,10 @@ void launch_construct(aco_gpu_ctx* c) {
         const int grid = std::max(1, std::min(c->mloc, per_sm * c->num_sms));
         c->construct_grid = grid;
         c->construct_desc = "k_construct_nn grid=" + std::to_string(grid);
+        if (fused_tail_enabled()) {
+            p.len_out = c->d_len;
+            c->fused_tail = true;
+        }
         k_construct_nn<<<grid, 32, smem1, c->stream>>>(p);
         check_launch(c, "k_construct_nn");
     } else {
@@ -495,7 +524,6 @@ void launch_construct(aco_gpu_ctx* c) {
     }
 }
 
-bool gather_mode(const aco_gpu_ctx* c) { return c->cfg.deposit != ACO_DEP_ACCUMULATE; }
 
 // construction + tour lengths + iteration stats (no host sync)
 void do_construct(aco_gpu_ctx* c) {
@@ -503,7 +531,7 @@ void do_construct(aco_gpu_ctx* c) {
     CK(cudaEventRecord(c->ev[0], c->stream));
     launch_construct(c);
     CK(cudaEventRecord(c->ev[1], c->stream));
-    {
+    if (!c->fused_tail) {
         const int warps = 8;
         const int grid = std::max(1, std::min((c->mloc + warps - 1) / warps, c->num_sms * 16));
         int32_t* succ = nullptr;

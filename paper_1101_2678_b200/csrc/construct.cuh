@@ -110,7 +110,57 @@ struct ConstructParams {
     int topk_k;
     int32_t* host_tours;        // device view of the caller's pinned tours_out (or null):
                                 // the roulette kernel streams each tour there as it grows
+    // fused tour tail (tour_tail): when len_out is set, the construction
+    // kernel itself forms C_k and 1/C_k (and succ/pred when set) and the
+    // separate k_tour_length launch is skipped
+    const int32_t* dist;        // n x P64
+    int64_t* len_out;           // mloc
+    double* inv_out;            // this rank's block of [world][S]
+    int32_t* succ_out;          // this rank's block of [world][n][S] (gather deposit) or null
+    int32_t* pred_out;
+    int S;
 };
+
+// Tour length (tour_length, model.hpp:205-226: an int64 sum, so any order is
+// exact), w_k = 1.0 / (double)C_k (inverse_lengths, pheromone.hpp:123-128)
+// and, for the row-gather deposit, the successor/predecessor tables — the
+// same results k_tour_length forms, computed in the construction kernel's
+// tail: the tour is read back from L2 right after it was built, eight edges
+// per lane in flight, while the other warps on the SM are still walking.
+// Plain loads for the tour (written by this kernel), __ldg for dist.
+__device__ __forceinline__ void tour_tail(const ConstructParams& p, const int32_t* tour, int kl, int lane) {
+    const int n = p.n;
+    long long acc = 0;
+    constexpr int B = 8;
+    for (int s0 = lane; s0 < n; s0 += 32 * B) {
+        int a[B], b[B], d[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int s = s0 + 32 * u;
+            a[u] = s < n ? tour[s] : 0;
+            b[u] = s < n ? tour[s + 1] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u)
+            d[u] = s0 + 32 * u < n ? __ldg(p.dist + static_cast<size_t>(a[u]) * p.P64 + b[u]) : 0;
+        if (p.succ_out) {
+#pragma unroll
+            for (int u = 0; u < B; ++u)
+                if (s0 + 32 * u < n) {
+                    p.succ_out[static_cast<size_t>(a[u]) * p.S + kl] = b[u];
+                    p.pred_out[static_cast<size_t>(b[u]) * p.S + kl] = a[u];
+                }
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) acc += d[u];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);
+    if (lane == 0) {
+        p.len_out[kl] = acc;
+        p.inv_out[kl] = 1.0 / static_cast<double>(acc);
+    }
+}
 
 // Streams a growing tour to mapped (pinned) host memory 32 entries at a time:
 // lane l holds entry 32c + l of the current 32-entry chunk c; a full chunk
@@ -893,6 +943,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
             hs.flush(p, kl, n, lane);
         }
         __syncwarp();
+        if (p.len_out) tour_tail(p, tour, kl, lane);
     }
 }
 
@@ -1257,6 +1308,7 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
             if (fb_full) atomicAdd(p.fallbacks, fb_full);
         }
         __syncwarp();
+        if (p.len_out) tour_tail(p, tour, kl, lane);
     }
 }
 
