@@ -577,22 +577,27 @@ __global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
 // always scans.  Rebuilt after every choice_info recomputation.
 //
 // Per row (one 256-thread CTA): 256 strided sub-range maxima straight from
-// the row (8 loads in flight per thread); M = the KT-th largest of them (by
-// rank), so at least KT cities have w >= M; a second pass over the row (L2-
-// resident by then) collects those cities, which are ranked by the total
-// order.  Bytes: 8 n^2 from HBM (+ the L2 re-read) + 4 KT n written.
+// the row (8 loads in flight per thread); M = the KT-th largest of their
+// high words (a 31-step bitwise search over block-wide counts), so at least
+// KT cities have w >= M; a second pass over the row (L2-resident by then)
+// collects those cities, which are ranked by the total order with integer
+// compares of the bit patterns (w >= 0, so they order like w).  Bytes: 8 n^2 from HBM (+ the L2 re-read) + 4 KT n written.
 constexpr int kTopK = 128;
 constexpr int kTopCap = 768;
+#ifndef ACO_TOPK_MINB
+#define ACO_TOPK_MINB 8 // CTAs per SM the register budget must allow
+#endif
+#ifndef ACO_TOPK_B
+#define ACO_TOPK_B 6 // row loads in flight per thread (8 spills at 32 registers)
+#endif
 
-__global__ void __launch_bounds__(256) k_row_topk(const double* __restrict__ choice, int n, int P64,
+__global__ void __launch_bounds__(256, ACO_TOPK_MINB) k_row_topk(const double* __restrict__ choice, int n, int P64,
                                                   int32_t* __restrict__ topk) {
-    __shared__ double smax[256];
-    __shared__ double cv[kTopCap];
-    __shared__ int ci[kTopCap];
+    // candidates as (bit pattern of w >= 0, which orders like w; index)
+    __shared__ ulonglong2 cand[kTopCap];
     __shared__ int s_cnt;
-    __shared__ double s_min[8];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int B = 8; // loads in flight per thread
+    const int tid = threadIdx.x;
+    constexpr int B = ACO_TOPK_B;
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
         const double* src = choice + static_cast<size_t>(i) * P64;
         if (tid == 0) s_cnt = 0;
@@ -608,21 +613,20 @@ __global__ void __launch_bounds__(256) k_row_topk(const double* __restrict__ cho
 #pragma unroll
             for (int u = 0; u < B; ++u) m0 = fmax(m0, v[u]);
         }
-        smax[tid] = m0;
-        __syncthreads();
-        // M = the KT-th largest sub-range maximum: >= KT cities have w >= M
-        double mine = 1e308;
-        {
-            int r = 0;
-            for (int q = 0; q < 256; ++q) r += smax[q] > m0 ? 1 : 0;
-            if (r < kTopK && m0 >= 0.0) mine = m0;
+        // M: the largest high word H (sign, exponent, 20 mantissa bits) such
+        // that >= KT sub-range maxima have high word >= H, found bit by bit
+        // with block-wide counts; M = H:0 is <= each of those maxima, so at
+        // least KT cities have w >= M.  (Fewer than KT non-empty sub-ranges,
+        // i.e. n < KT: M = 0 and every city is a candidate.)
+        const bool valid = m0 >= 0.0;
+        const uint32_t hi = valid ? static_cast<uint32_t>(__double_as_longlong(m0) >> 32) : 0u;
+        uint32_t H = 0;
+#pragma unroll 1
+        for (int bit = 30; bit >= 0; --bit) {
+            const uint32_t c = H | (1u << bit);
+            if (__syncthreads_count(valid && hi >= c) >= kTopK) H = c;
         }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) mine = fmin(mine, __shfl_xor_sync(kFull, mine, off));
-        if (lane == 0) s_min[warp] = mine;
-        __syncthreads();
-        double M = s_min[0];
-        for (int w = 1; w < 8; ++w) M = fmin(M, s_min[w]);
+        const double M = __longlong_as_double(static_cast<long long>(H) << 32);
         // second pass over the (now L2-resident) row: collect w >= M
         for (int k0 = 0; k0 < n; k0 += 256 * B) {
             double v[B];
@@ -635,10 +639,9 @@ __global__ void __launch_bounds__(256) k_row_topk(const double* __restrict__ cho
             for (int u = 0; u < B; ++u) {
                 if (v[u] >= M) {
                     const int pos = atomicAdd(&s_cnt, 1);
-                    if (pos < kTopCap) {
-                        cv[pos] = v[u];
-                        ci[pos] = k0 + 256 * u + tid;
-                    }
+                    if (pos < kTopCap)
+                        cand[pos] = make_ulonglong2(static_cast<unsigned long long>(__double_as_longlong(v[u])),
+                                                    static_cast<unsigned long long>(k0 + 256 * u + tid));
                 }
             }
         }
@@ -648,15 +651,15 @@ __global__ void __launch_bounds__(256) k_row_topk(const double* __restrict__ cho
         if (c > kTopCap) {
             if (tid == 0) out[0] = -2; // invalid: the construction scans the row
         } else {
+            // rank under (w desc, index asc), branch-free integer compares
             for (int a = tid; a < c; a += 256) {
-                const double va = cv[a];
-                const int ja = ci[a];
+                const ulonglong2 ea = cand[a];
                 int r = 0;
                 for (int b = 0; b < c; ++b) {
-                    const double vb = cv[b];
-                    r += (vb > va || (vb == va && ci[b] < ja)) ? 1 : 0;
+                    const ulonglong2 eb = cand[b];
+                    r += static_cast<int>((eb.x > ea.x) | ((eb.x == ea.x) & (eb.y < ea.y)));
                 }
-                if (r < kTopK) out[r] = ja;
+                if (r < kTopK) out[r] = static_cast<int32_t>(ea.y);
             }
             for (int r = c + tid; r < kTopK; r += 256) out[r] = -1; // n < KT: end of list
         }
