@@ -169,6 +169,11 @@ aco_status aco_gpu_get_choice(aco_gpu_ctx* ctx, double* choice);
 /* choice32 as the construction kernel streams it, de-permuted and unscaled
  * (diagnostic; ACO_E_UNSUPPORTED when the fp32 stream is off). */
 aco_status aco_gpu_get_choice32(aco_gpu_ctx* ctx, float* choice, int32_t* row_scale_exp);
+/* nn selection's per-row argmax cache (diagnostic): n x 128 city ids, the
+ * row's best cities under (choice desc, index asc); -1 ends a short list,
+ * entry 0 = -2 marks a row the construction always scans in full.
+ * ACO_E_UNSUPPORTED when the cache is off (roulette, or ACO_NN_TOPK=0). */
+aco_status aco_gpu_get_topk(aco_gpu_ctx* ctx, int32_t* topk, int32_t* k);
 aco_status aco_gpu_get_tours(aco_gpu_ctx* ctx, int32_t* tours, int64_t* lengths);
 aco_status aco_gpu_get_best(aco_gpu_ctx* ctx, int32_t* tour, int64_t* length);
 /* Resolved configuration: m (after m=0 -> n), local ant range, tau0, stream. */

@@ -57,7 +57,7 @@ EXPORTS = [
     "aco_predicted_access_cost", "aco_last_error", "aco_gpu_create", "aco_gpu_destroy",
     "aco_gpu_last_error", "aco_gpu_set_pheromone", "aco_gpu_compute_choice_info",
     "aco_gpu_construct", "aco_gpu_update", "aco_gpu_iterate", "aco_gpu_get_pheromone",
-    "aco_gpu_get_choice", "aco_gpu_get_choice32", "aco_gpu_get_tours", "aco_gpu_get_best",
+    "aco_gpu_get_choice", "aco_gpu_get_choice32", "aco_gpu_get_topk", "aco_gpu_get_tours", "aco_gpu_get_best",
     "aco_gpu_get_info", "aco_gpu_stream", "aco_gpu_exchange_buffers", "aco_gpu_launch_count", "aco_gpu_describe", "aco_gpu_nccl_unique_id",
     "aco_gpu_philox_uniform",
 ]
@@ -96,6 +96,7 @@ def _load() -> C.CDLL:
     L.aco_gpu_get_pheromone.argtypes = [_p, _p]
     L.aco_gpu_get_choice.argtypes = [_p, _p]
     L.aco_gpu_get_choice32.argtypes = [_p, _p, _p]
+    L.aco_gpu_get_topk.argtypes = [_p, _p, C.POINTER(_i32)]
     L.aco_gpu_get_tours.argtypes = [_p, _p, _p]
     L.aco_gpu_get_best.argtypes = [_p, _p, C.POINTER(C.c_int64)]
     L.aco_gpu_get_info.argtypes = [_p, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32),

@@ -374,6 +374,15 @@ class Engine:
         _check(lib.aco_gpu_get_choice32(self._h, ptr(out), ptr(sc)), self._h)
         return out, sc
 
+    def topk(self) -> np.ndarray:
+        """nn selection's per-row argmax cache [n, K] (diagnostic; see
+        aco_gpu_get_topk)."""
+        k = C.c_int32(0)
+        _check(lib.aco_gpu_get_topk(self._h, None, C.byref(k)), self._h)
+        out = np.zeros((self._n, k.value), np.int32)
+        _check(lib.aco_gpu_get_topk(self._h, ptr(out), None), self._h)
+        return out
+
     def ants(self):
         """(tours[m_local, n+1], lengths[m_local]) of the last construction."""
         k = self.ant_end - self.ant_begin

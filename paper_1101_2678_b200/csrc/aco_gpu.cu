@@ -426,12 +426,12 @@ ConstructParams make_cp(aco_gpu_ctx* c) {
     return p;
 }
 
-// the roulette and nn kernels form the tour lengths in their tail
-// (tour_tail); ACO_FUSED_TAIL=0 keeps the separate k_tour_length launch
+// the nn kernel forms the tour lengths in its tail (tour_tail);
+// ACO_FUSED_TAIL=0 keeps the separate k_tour_length launch
 bool fused_tail_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("ACO_FUSED_TAIL");
-        return !(e && e[0] == '0');
+        return ACO_FUSED_TAIL_BUILD && !(e && e[0] == '0');
     }();
     return on;
 }
@@ -493,10 +493,6 @@ void launch_construct(aco_gpu_ctx* c) {
                             (st ? " streams_tours_to_host" : "");
         if (std::getenv("ACO_DEBUG"))
             std::fprintf(stderr, "construct: %s\n", c->construct_desc.c_str());
-        if (fused_tail_enabled()) {
-            p.len_out = c->d_len;
-            c->fused_tail = true;
-        }
         fn<<<grid, 32, smem, c->stream>>>(p);
         check_launch(c, "k_construct_roulette");
     } else if (c->cfg.selection == ACO_SEL_NN) {
@@ -1102,6 +1098,18 @@ aco_status aco_gpu_get_choice(aco_gpu_ctx* c, double* choice) {
         CK(cudaSetDevice(c->device));
         CK(cudaMemcpy2DAsync(choice, c->n * sizeof(double), c->d_choice, c->P64 * sizeof(double),
                              c->n * sizeof(double), c->n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+aco_status aco_gpu_get_topk(aco_gpu_ctx* c, int32_t* topk, int32_t* k) {
+    return guard_ctx(c, [&] {
+        if (!c->d_topk) throw Fail{ACO_E_UNSUPPORTED, "argmax cache not active"};
+        CK(cudaSetDevice(c->device));
+        if (k) *k = kTopK;
+        if (topk)
+            CK(cudaMemcpyAsync(topk, c->d_topk, static_cast<size_t>(c->n) * kTopK * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
     });
 }

@@ -89,6 +89,10 @@ __host__ __device__ __forceinline__ int stream_city(int p, int C, int V, int LA 
     return r * LA * C + l * C + t * V + q;
 }
 
+#ifndef ACO_FUSED_TAIL_BUILD
+#define ACO_FUSED_TAIL_BUILD 1 // 0: the kernels carry no tail (k_tour_length always runs)
+#endif
+
 struct ConstructParams {
     const void* w;           // streamed weights (float or double), row pitch PW
     const double* w64;       // natural fp64 choice, row pitch P64 (exact walk, nn)
@@ -110,9 +114,11 @@ struct ConstructParams {
     int topk_k;
     int32_t* host_tours;        // device view of the caller's pinned tours_out (or null):
                                 // the roulette kernel streams each tour there as it grows
-    // fused tour tail (tour_tail): when len_out is set, the construction
-    // kernel itself forms C_k and 1/C_k (and succ/pred when set) and the
-    // separate k_tour_length launch is skipped
+    // fused tour tail (tour_tail, nn kernel): when len_out is set, the
+    // construction kernel itself forms C_k and 1/C_k (and succ/pred when
+    // set) and the separate k_tour_length launch is skipped.  (The roulette
+    // kernel does not carry it: at 96 registers the extra code costs its
+    // walk ~2.5%, more than the k_tour_length launch it would save.)
     const int32_t* dist;        // n x P64
     int64_t* len_out;           // mloc
     double* inv_out;            // this rank's block of [world][S]
@@ -943,7 +949,6 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
             hs.flush(p, kl, n, lane);
         }
         __syncwarp();
-        if (p.len_out) tour_tail(p, tour, kl, lane);
     }
 }
 
@@ -1308,7 +1313,7 @@ __global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
             if (fb_full) atomicAdd(p.fallbacks, fb_full);
         }
         __syncwarp();
-        if (p.len_out) tour_tail(p, tour, kl, lane);
+        if (ACO_FUSED_TAIL_BUILD && p.len_out) tour_tail(p, tour, kl, lane);
     }
 }
 

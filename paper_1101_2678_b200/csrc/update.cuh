@@ -44,31 +44,30 @@ __global__ void k_tour_length(const int32_t* __restrict__ tours, const int32_t* 
     for (int kl = blockIdx.x * warps + (threadIdx.x >> 5); kl < mloc; kl += gridDim.x * warps) {
         const int32_t* t = tours + static_cast<size_t>(kl) * (n + 1);
         long long acc = 0;
-        if (!succ) {
-            // lengths only: batches of 8 edges per lane, all (random)
-            // distance gathers of a batch in flight together
-            constexpr int B = 8;
-            for (int s0 = lane; s0 < n; s0 += 32 * B) {
-                int a[B], b[B], d[B];
+        // batches of 8 edges per lane: all (random) distance gathers of a
+        // batch in flight together; the succ/pred scatter stores after them
+        constexpr int B = 8;
+        for (int s0 = lane; s0 < n; s0 += 32 * B) {
+            int a[B], b[B], d[B];
 #pragma unroll
-                for (int u = 0; u < B; ++u) {
-                    const int s = s0 + 32 * u;
-                    a[u] = s < n ? t[s] : 0;
-                    b[u] = s < n ? t[s + 1] : 0;
-                }
+            for (int u = 0; u < B; ++u) {
+                const int s = s0 + 32 * u;
+                a[u] = s < n ? t[s] : 0;
+                b[u] = s < n ? t[s + 1] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < B; ++u)
+                d[u] = s0 + 32 * u < n ? __ldg(dist + static_cast<size_t>(a[u]) * P64 + b[u]) : 0;
+            if (succ) {
 #pragma unroll
                 for (int u = 0; u < B; ++u)
-                    d[u] = s0 + 32 * u < n ? __ldg(dist + static_cast<size_t>(a[u]) * P64 + b[u]) : 0;
+                    if (s0 + 32 * u < n) {
+                        succ[static_cast<size_t>(a[u]) * S + kl] = b[u];
+                        pred[static_cast<size_t>(b[u]) * S + kl] = a[u];
+                    }
+            }
 #pragma unroll
-                for (int u = 0; u < B; ++u) acc += d[u];
-            }
-        } else {
-            for (int s = lane; s < n; s += 32) {
-                const int a = t[s], b = t[s + 1];
-                acc += dist[static_cast<size_t>(a) * P64 + b];
-                succ[static_cast<size_t>(a) * S + kl] = b;
-                pred[static_cast<size_t>(b) * S + kl] = a;
-            }
+            for (int u = 0; u < B; ++u) acc += d[u];
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);

@@ -281,6 +281,51 @@ def test_nn_argmax_cache_bit_exact(aco, oracle, monkeypatch, topk):
             assert fields["topk"] == "off" and full == argmax
 
 
+def _expected_topk(choice, k):
+    n = choice.shape[0]
+    out = np.full((n, k), -1, np.int32)
+    idx = np.arange(n)
+    for i in range(n):
+        order = np.lexsort((idx, -choice[i]))[:k]  # (w desc, index asc)
+        out[i, :len(order)] = order
+    return out
+
+
+@pytest.mark.parametrize("n,pattern", [(1500, "uniform"), (1500, "loguniform"),
+                                       (2392, "ties"), (100, "uniform"), (300, "loguniform")])
+def test_nn_topk_lists_exact(aco, n, pattern):
+    """k_row_topk's lists equal the exact top-K under (choice desc, index
+    asc) of the device choice rows: uniform tau (eta ties from integer
+    distances), log-uniform tau over 2^-100..1 (exponents spread across the
+    threshold search), tau from 3 values (heavy ties), and n < K (the list
+    ends with -1).  A row may only be marked -2 (full scan) when more than
+    768 of its cities tie at or above its K-th value's 2^-20 band."""
+    prob, eng = make(aco, n, selection=1, deposit=0, nn=8, ant_range=(0, 1))
+    rng = np.random.default_rng(n)
+    with eng:
+        if pattern == "uniform":
+            tau = np.full((n, n), eng.tau0)
+        elif pattern == "loguniform":
+            tau = np.exp2(-100.0 * rng.random((n, n)))
+        else:
+            tau = rng.choice([1.0, 0.5, 0.25], size=(n, n))
+        tau = np.minimum(tau, tau.T)  # symmetric like the colony's
+        eng.set_pheromone(tau)
+        eng.compute_choice_info()
+        ch = eng.choice()
+        got = eng.topk()
+    K = got.shape[1]
+    assert K == 128
+    exp = _expected_topk(ch, K)
+    bad = got[:, 0] == -2
+    for i in np.nonzero(bad)[0]:
+        kth = np.sort(ch[i])[::-1][K - 1]
+        assert np.count_nonzero(ch[i] >= kth * (1 - 2.0 ** -20)) > 768, f"row {i} flagged without overflow"
+    assert np.array_equal(got[~bad], exp[~bad])
+    if pattern != "ties":
+        assert not bad.any()
+
+
 def test_gather_cta_row_kernel_bit_exact(aco, oracle):
     """n = 4500: a row of doubles no longer fits one warp's shared slice, so
     the gather update runs the CTA-per-row k_rows<GATHER> (paired, batched
