@@ -500,7 +500,8 @@ void launch_construct(aco_gpu_ctx* c) {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_construct_nn, 32, smem1));
         const int grid = std::max(1, std::min(c->mloc, per_sm * c->num_sms));
         c->construct_grid = grid;
-        c->construct_desc = "k_construct_nn grid=" + std::to_string(grid);
+        c->construct_desc = "k_construct_nn grid=" + std::to_string(grid) +
+                            " per_sm=" + std::to_string(per_sm);
         if (fused_tail_enabled()) {
             p.len_out = c->d_len;
             c->fused_tail = true;
