@@ -1015,7 +1015,10 @@ __global__ void __launch_bounds__(32) k_construct_roulette_exact(ConstructParams
 // is the exact (value, lowest index) argmax over all unvisited cities
 // (construction.hpp:108-120), which consumes no draw; it streams the fp64
 // row with 8 independent 16-byte loads per lane in flight.
-__global__ void __launch_bounds__(32, 16) k_construct_nn(ConstructParams p) {
+#ifndef ACO_NN_MINB
+#define ACO_NN_MINB 16 // resident warps per SM the register budget must allow
+#endif
+__global__ void __launch_bounds__(32, ACO_NN_MINB) k_construct_nn(ConstructParams p) {
     extern __shared__ uint32_t smem_tabu[];
     uint32_t* tabu = smem_tabu;
     const int lane = threadIdx.x & 31;
