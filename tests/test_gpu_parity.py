@@ -281,6 +281,55 @@ def test_nn_argmax_cache_bit_exact(aco, oracle, monkeypatch, topk):
             assert fields["topk"] == "off" and full == argmax
 
 
+_TAIL_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1101_2678_b200 import aco
+prob = aco.build_problem(aco.synthetic_instance(700))
+for dep in (0, 1):
+    cfg = aco.RunConfig(params=aco.Parameters(m=64, nn=12, seed=4),
+                        selection=aco.SelectionStrategy(aco.Selection.roulette_nn),
+                        deposit=aco.DepositStrategy(aco.Deposit(dep)))
+    with aco.Engine(prob, cfg) as eng:
+        for _ in range(3 if dep else 1):  # atomic tau is order-nondeterministic
+            eng.run_iteration()
+        t, l = eng.ants()
+        np.save(sys.argv[2] + f"_{dep}_tours.npy", t)
+        np.save(sys.argv[2] + f"_{dep}_lens.npy", l)
+        np.save(sys.argv[2] + f"_{dep}_tau.npy", eng.pheromone())
+        print(eng.describe())
+"""
+
+
+def test_nn_tour_tail_matches_k_tour_length(tmp_path):
+    """The nn kernel's fused tour tail (C_k, 1/C_k, succ/pred) and the
+    separate k_tour_length launch (ACO_FUSED_TAIL=0, read once per process,
+    hence the subprocesses) give identical tours, lengths and — for the
+    gather deposit, which reads succ/pred and 1/C_k — bit-identical tau
+    over three iterations (the atomic deposit: one iteration, tau within
+    1e-5)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for v in ("1", "0"):
+        env = dict(os.environ, ACO_FUSED_TAIL=v)
+        r = subprocess.run([sys.executable, "-c", _TAIL_SCRIPT, root, str(tmp_path / v)],
+                           env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[v] = {dep: [np.load(tmp_path / f"{v}_{dep}_{k}.npy") for k in ("tours", "lens", "tau")]
+                  for dep in (0, 1)}
+    for dep in (0, 1):
+        a, b = out["1"][dep], out["0"][dep]
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        if dep == 1:
+            assert np.array_equal(a[2], b[2])
+        else:
+            assert np.max(np.abs(a[2] - b[2]) / b[2]) <= 1e-5
+
+
 def _expected_topk(choice, k):
     n = choice.shape[0]
     out = np.full((n, k), -1, np.int32)
