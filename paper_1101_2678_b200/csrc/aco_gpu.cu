@@ -128,6 +128,7 @@ struct aco_gpu_ctx {
     int32_t* d_succ = nullptr; // [world][n][S]
     int32_t* d_pred = nullptr;
     double* d_delta = nullptr;
+    float* d_delta32 = nullptr; // sharded atomic path over NCCL: the fp32 wire copy of d_delta
     long long* d_stats = nullptr;   // [0..2] stats, [3] best_so_far
     int32_t* d_best = nullptr;      // n+1
     unsigned long long* d_fb = nullptr; // [0] roulette fallbacks, [1] nn argmax fallbacks
@@ -326,6 +327,7 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
     rp.lut = c->d_lut;
     rp.etab = c->d_etab;
     rp.delta = c->d_delta;
+    rp.delta32 = c->d_delta32;
     rp.succ = c->d_succ;
     rp.pred = c->d_pred;
     rp.inv = c->d_inv;
@@ -379,9 +381,11 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
         CK(cudaFuncSetAttribute(k_rows<MODE_CHOICE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute(k_rows<MODE_GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute(k_rows<MODE_DELTA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k_rows<MODE_DELTA32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
     if (mode == MODE_CHOICE) k_rows<MODE_CHOICE><<<grid, 256, rsmem, c->stream>>>(rp);
     else if (mode == MODE_GATHER) k_rows<MODE_GATHER><<<grid, 256, rsmem, c->stream>>>(rp);
+    else if (mode == MODE_DELTA32) k_rows<MODE_DELTA32><<<grid, 256, rsmem, c->stream>>>(rp);
     else k_rows<MODE_DELTA><<<grid, 256, rsmem, c->stream>>>(rp);
     check_launch(c, "k_rows");
     launch_topk(c);
@@ -570,8 +574,16 @@ void do_update(aco_gpu_ctx* c) {
                              ncclFloat64, c->comm, c->stream));
             NK(api.GroupEnd());
         } else {
-            NK(api.AllReduce(c->d_delta, c->d_delta, static_cast<size_t>(c->n) * c->P64,
-                             ncclFloat64, ncclSum, c->comm, c->stream));
+            const size_t cells = static_cast<size_t>(c->n) * c->P64;
+            if (c->d_delta32) {
+                k_delta_pack<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_delta, c->d_delta32, cells / 2);
+                check_launch(c, "k_delta_pack");
+                NK(api.AllReduce(c->d_delta32, c->d_delta32, cells, ncclFloat32, ncclSum, c->comm,
+                                 c->stream));
+            } else {
+                NK(api.AllReduce(c->d_delta, c->d_delta, cells, ncclFloat64, ncclSum, c->comm,
+                                 c->stream));
+            }
         }
     }
     CK(cudaEventRecord(c->ev[3], c->stream));
@@ -579,7 +591,7 @@ void do_update(aco_gpu_ctx* c) {
         launch_rows(c, MODE_GATHER);
         CK(cudaEventRecord(c->ev[4], c->stream));
     } else if (c->sharded) {
-        launch_rows(c, MODE_DELTA);
+        launch_rows(c, (c->d_delta32 && !c->external) ? MODE_DELTA32 : MODE_DELTA);
         CK(cudaEventRecord(c->ev[4], c->stream));
     } else {
         const size_t count2 = static_cast<size_t>(c->n) * c->P64 / 2;
@@ -870,6 +882,10 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
             (warp_gather && !(gsplit && gsplit[0] == '0'))) {
             CK(cudaMalloc(&c->d_delta, cells * sizeof(double)));
             CK(cudaMemset(c->d_delta, 0, cells * sizeof(double)));
+            const char* wire = std::getenv("ACO_WIRE_FP64"); // "1": all-reduce the fp64 delta
+            if (c->sharded && !c->external && c->cfg.deposit == ACO_DEP_ACCUMULATE &&
+                !(wire && wire[0] == '1'))
+                CK(cudaMalloc(&c->d_delta32, cells * sizeof(float)));
         }
         CK(cudaMalloc(&c->d_stats, 8 * sizeof(long long)));
         const long long init_stats[8] = {0, 0, 0, LLONG_MAX, 0, 0, 0, 0};
@@ -932,7 +948,7 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
     if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
     void* bufs[] = {c->d_choice_nn, c->d_choice_nn32, c->d_nn_scale, c->d_topk, c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
                     c->d_choice_p64, c->d_scale, c->d_nn, c->d_tours, c->d_len, c->d_inv,
-                    c->d_succ, c->d_pred, c->d_delta, c->d_stats, c->d_best, c->d_fb, c->d_tourbuf};
+                    c->d_succ, c->d_pred, c->d_delta, c->d_delta32, c->d_stats, c->d_best, c->d_fb, c->d_tourbuf};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_stats) cudaFreeHost(c->h_stats);

@@ -182,6 +182,22 @@ __global__ void k_evaporate(double* __restrict__ tau, size_t count2, double keep
     }
 }
 
+// Multi-GPU atomic path, NCCL wire in fp32: the local fp64 delta (summed
+// by red.f64) is rounded once to fp32 for the all-reduce and zeroed for the
+// next iteration.  Half the exchange bytes; the rounding (2^-24 relative,
+// plus the G-term fp32 sum inside NCCL) stays far inside the path's 1e-5
+// relative tau tolerance, and every rank receives the same reduced value.
+__global__ void k_delta_pack(double* __restrict__ delta, float* __restrict__ d32, size_t count2) {
+    double2* d2 = reinterpret_cast<double2*>(delta);
+    float2* f2 = reinterpret_cast<float2*>(d32);
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count2;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const double2 v = d2[i];
+        f2[i] = make_float2(__double2float_rn(v.x), __double2float_rn(v.y));
+        d2[i] = make_double2(0.0, 0.0);
+    }
+}
+
 // One thread per (ant, step); edges (t[s], t[s+1]) and the mirror.
 __global__ void k_deposit_atomic(const int32_t* __restrict__ tours, const double* __restrict__ inv,
                                  int n, int P64, int mloc, double* __restrict__ target) {
@@ -197,7 +213,9 @@ __global__ void k_deposit_atomic(const int32_t* __restrict__ tours, const double
     }
 }
 
-enum { MODE_CHOICE = 0, MODE_GATHER = 1, MODE_DELTA = 2 };
+// MODE_DELTA32: MODE_DELTA reading the fp32 all-reduced delta (NCCL fp32
+// wire; k_delta_pack already zeroed the fp64 delta)
+enum { MODE_CHOICE = 0, MODE_GATHER = 1, MODE_DELTA = 2, MODE_DELTA32 = 3 };
 
 struct RowParams {
     double* tau;             // n x P64
@@ -209,6 +227,7 @@ struct RowParams {
     const double* lut;       // eta^beta by distance, or null
     const double* etab;      // n x P64 eta^beta, or null
     double* delta;           // MODE_DELTA: n x P64
+    const float* delta32;    // MODE_DELTA32: n x P64
     const int32_t* succ;     // MODE_GATHER: [shard][city][S]
     const int32_t* pred;
     const double* inv;       // [shard][S]
@@ -368,6 +387,12 @@ __global__ void __launch_bounds__(256, 3) k_rows(RowParams p) {
                 tv[u] = in ? trow2[j2] : make_double2(0.0, 0.0);
                 dv[u] = (in && !erow2) ? __ldg(drow2 + j2) : make_int2(0, 0);
                 if constexpr (MODE == MODE_DELTA) dl[u] = in ? drw2[j2] : make_double2(0.0, 0.0);
+                if constexpr (MODE == MODE_DELTA32) {
+                    const float2 f = in ? reinterpret_cast<const float2*>(
+                                              p.delta32 + static_cast<size_t>(i) * p.P64)[j2]
+                                        : make_float2(0.f, 0.f);
+                    dl[u] = make_double2(f.x, f.y);
+                }
                 if constexpr (MODE == MODE_GATHER) {
                     dl[u] = in ? reinterpret_cast<const double2*>(rowbuf)[j2] : make_double2(0.0, 0.0);
                 }
@@ -386,7 +411,7 @@ __global__ void __launch_bounds__(256, 3) k_rows(RowParams p) {
                 if (j2 < n2) {
                     const int j = 2 * j2;
                     double2 t = tv[u];
-                    if constexpr (MODE == MODE_GATHER || MODE == MODE_DELTA) {
+                    if constexpr (MODE == MODE_GATHER || MODE == MODE_DELTA || MODE == MODE_DELTA32) {
                         // pheromone.hpp:183 (evaporate) then :220 / the summed delta
                         t.x = __dadd_rn(__dmul_rn(t.x, p.keep), dl[u].x);
                         t.y = __dadd_rn(__dmul_rn(t.y, p.keep), dl[u].y);

@@ -21,7 +21,9 @@ Rooflines:
   update (accumulate, G=1): evaporate 16*n*P + deposit 2*m*n red.f64 (8 B each)
       + tours 4*m*(n+1) + choice epilogue (8+4+8+S)*n*P, over HBM peak;
   update (accumulate, G>1): k_rows<DELTA> (8+8+8+8+4+8+S)*n*P (the local
-      red.f64 deposit runs in the construction phase);
+      red.f64 deposit runs in the construction phase; shard emulation runs
+      the fp64 external-exchange kernel — the NCCL path's k_delta_pack +
+      k_rows<DELTA32> are timed separately by tools/pack_cost.py);
   update (gather):         (8+8+4+8+S)*n*P + 16*m*n + 8*m, over HBM peak;
   S = 4 for the roulette's fp32 stream, 0 for nn; nn adds the top-K rebuild's
       8*n*P re-read of the choice rows.
@@ -133,9 +135,9 @@ def exchange_model(n, m_total, G, deposit):
         return None
     P = (n + 31) // 32 * 32
     if deposit == 0:
-        size = n * P * 8
+        size = n * P * 4  # fp32 wire (k_delta_pack), DESIGN §5
         wire = 2 * (G - 1) / G * size
-        what = f"ncclAllReduce(delta, {n}x{P} f64, sum)"
+        what = f"ncclAllReduce(delta, {n}x{P} f32, sum) after k_delta_pack"
     else:
         S = -(-m_total // G)
         size = G * (2 * n * S * 4 + S * 8)
