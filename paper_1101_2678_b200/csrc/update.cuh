@@ -611,6 +611,9 @@ constexpr int kTopCap = 768;
 #ifndef ACO_TOPK_MINB
 #define ACO_TOPK_MINB 8 // CTAs per SM the register budget must allow
 #endif
+#ifndef ACO_TOPK_REFINE
+#define ACO_TOPK_REFINE 1 // second threshold over the candidates before ranking
+#endif
 #ifndef ACO_TOPK_B
 #define ACO_TOPK_B 6 // row loads in flight per thread (8 spills at 32 registers)
 #endif
@@ -670,11 +673,32 @@ __global__ void __launch_bounds__(256, ACO_TOPK_MINB) k_row_topk(const double* _
             }
         }
         __syncthreads();
-        const int c = s_cnt;
+        int c = s_cnt;
         int32_t* out = topk + static_cast<size_t>(i) * kTopK;
         if (c > kTopCap) {
             if (tid == 0) out[0] = -2; // invalid: the construction scans the row
         } else {
+#if ACO_TOPK_REFINE
+            if (c > kTopK + 16 && c <= 256) {
+                // second threshold, over the candidates' own high words: a
+                // candidate below H2 is below every candidate at or above
+                // it, and >= KT are at or above, so only those are ranked
+                const bool own = tid < c;
+                const ulonglong2 e = own ? cand[tid] : make_ulonglong2(0ull, 0ull);
+                const uint32_t h = static_cast<uint32_t>(e.x >> 32);
+                uint32_t H2 = 0;
+#pragma unroll 1
+                for (int bit = 30; bit >= 0; --bit) {
+                    const uint32_t cnd = H2 | (1u << bit);
+                    if (__syncthreads_count(own && h >= cnd) >= kTopK) H2 = cnd;
+                }
+                if (tid == 0) s_cnt = 0;
+                __syncthreads();
+                if (own && h >= H2) cand[atomicAdd(&s_cnt, 1)] = e;
+                __syncthreads();
+                c = s_cnt;
+            }
+#endif
             // rank under (w desc, index asc), branch-free integer compares
             for (int a = tid; a < c; a += 256) {
                 const ulonglong2 ea = cand[a];
