@@ -38,6 +38,18 @@ sys.path.insert(0, ROOT)
 
 METRIC = "ms per ACO iteration (construct+update) at pr2392, m=n ants, 1/2/4/8 B200"
 N_CITIES = 2392
+DATA = "synthetic (SURVEY App. B generator, pr2392-size EUC_2D)"
+
+
+def workload_config(world: int) -> dict:
+    """The `config` object of BOTH arms (identical for the same N, so the
+    driver's same_config check compares like with like)."""
+    return {"workload": "pr2392 m=n roulette + accumulate (atomic) deposit",
+            "n": N_CITIES, "m": N_CITIES, "alpha": 1.0, "beta": 2.0, "rho": 0.5, "seed": 1,
+            "selection": "roulette", "deposit": "accumulate",
+            "parallelism": f"ant-sharded x{world}" if world > 1 else "single device",
+            "l2": "GPU arm: L2 flushed (512 MiB write on the engine stream) before every "
+                  "timed iteration, device-timed and e2e alike"}
 
 
 def env_rank():
@@ -175,8 +187,8 @@ def run_reference_arm(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    steps = max(1, min(args.steps, 5))
-    warm = min(args.warmup, 1)
+    steps = args.steps  # the GPU arm's K and W (1.3-1.7 s per reference iteration)
+    warm = args.warmup
     t0 = time.time()
     ref = cpu_reference_time(N_CITIES, steps, warm)
     wall = time.time() - t0
@@ -190,10 +202,9 @@ def run_reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": ref["value"], "unit": "ms",
         "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": ref["value"],
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (SURVEY App. B generator)",
-        "config": {"workload": "pr2392 m=n roulette + accumulate (atomic) deposit",
-                   "n": N_CITIES, "m": N_CITIES, "alpha": 1.0, "beta": 2.0, "rho": 0.5,
-                   "seed": 1, "parallelism": f"reference ThreadPool x{ref['cores']} host threads"},
+        "data": DATA,
+        "config": workload_config(args.gpus),
+        "host": f"reference ThreadPool x{ref['cores']} host threads",
         "cpu_baseline": {"value": ref["value"], "unit": "ms", "cores": ref["cores"],
                          "kind": "reference",
                          "sample": f"{steps} full reference iterations after {warm} warm-up "
@@ -215,7 +226,9 @@ def run_ours(args):
 
     rank, world, local = env_rank()
     if world != args.gpus:
-        world = args.gpus if world == 1 else world
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks but {torch.cuda.device_count()} visible GPUs")
     device = local if torch.cuda.device_count() > 1 else 0
     torch.cuda.set_device(device)
     from paper_1101_2678_b200 import aco
@@ -223,6 +236,10 @@ def run_ours(args):
     dist_on = world > 1
     if dist_on:
         import torch.distributed as dist
+
+        # NCCL's communicator lines (nRanks per comm) in the log, for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", device))
 
@@ -297,9 +314,13 @@ def run_ours(args):
     tours_h = torch.empty((mloc, N_CITIES + 1), dtype=torch.int32, pin_memory=True).numpy()
     lens_h = torch.empty(mloc, dtype=torch.int64, pin_memory=True).numpy()
     e2e = []
+    sp = torch.cuda.ExternalStream(eng.stream_handle(), device=f"cuda:{device}")
     if dist_on:
         dist.barrier()
     for _ in range(args.steps):
+        with torch.cuda.stream(sp):
+            flush.fill_(rank & 0xFF)  # evict L2 before every timed iteration here too
+        sp.synchronize()
         t0 = time.perf_counter()
         eng.run_iteration(tours_out=tours_h, lengths_out=lens_h)
         e2e.append((time.perf_counter() - t0) * 1e3)
@@ -366,12 +387,9 @@ def run_ours(args):
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (SURVEY App. B generator, pr2392-size EUC_2D)",
-        "config": {"workload": "pr2392 m=n roulette + accumulate (atomic) deposit",
-                   "n": n, "m": m, "alpha": 1.0, "beta": 2.0, "rho": 0.5, "seed": 1,
-                   "weight_stream": "fp32 row-scaled filter + fp64 certification/exact fallback",
-                   "parallelism": f"ant-sharded x{world}" if world > 1 else "1 GPU",
-                   "l2": "flushed between timed iterations (512 MiB write on the engine stream)"},
+        "data": DATA,
+        "config": workload_config(world),
+        "weight_stream": "fp32 row-scaled filter + fp64 certification/exact fallback",
         "construct_ms": round(construct_ms, 4), "construct_kernel_ms": round(kernel_ms, 4),
         "update_ms": round(update_ms, 4), "exchange_ms": round(exch_ms, 4),
         "choice_ms": round(choice_ms, 4), "fallback_steps_per_iter": fallbacks,
@@ -429,6 +447,25 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def respawn_under_torchrun(gpus: int):
+    """`python bench.py --gpus N` outside torchrun: re-run this command as N
+    ranks (one process per GPU) under torch.distributed.run on 127.0.0.1,
+    exactly as the driver's own launch does; the exit code is torchrun's."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -437,7 +474,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        respawn_under_torchrun(args.gpus)
     if args.impl == "reference":
         run_reference_arm(args)
     else:

@@ -105,7 +105,22 @@ typedef struct {
     int32_t rank, world;
     int32_t ant_begin, ant_end;
     uint8_t nccl_id[128];
+    /* Datatype of the sharded accumulate path's delta-tau all-reduce:
+     * ACO_WIRE_FP64 (default) keeps the reference's fp64 reals end to end
+     * (ranks differ from a single-GPU colony only by the atomic order,
+     * ~1e-16); ACO_WIRE_FP32 halves the wire bytes at one 2^-24 rounding of
+     * every delta per iteration, so tours after iteration 0 may then depend
+     * on the GPU count.  Every rank of a colony must pass the same value. */
+    int32_t wire;
+    /* Debug mode (TourBuffer::make pheromone.hpp:67-90 and
+     * tour_length model.hpp:205-220): every construction is followed by a
+     * device check that each tour is closed, a permutation of 0..n-1 and of
+     * the stored length; a violation fails the call with ACO_E_NOT_CLOSED /
+     * ACO_E_NOT_A_PERMUTATION / ACO_E_INCONSISTENT_LENGTH.  Off by default. */
+    int32_t validate_tours;
 } aco_gpu_params;
+
+enum { ACO_WIRE_FP64 = 0, ACO_WIRE_FP32 = 1 };
 
 /* aco::IterationRecord (engine.hpp:31-38) + device timings. */
 typedef struct {
@@ -119,8 +134,11 @@ typedef struct {
     double construct_kernel_ms; /* the construction kernel alone */
     double ledger[4];      /* predicted_access_cost: global_loads, global_stores,
                               shared_loads, atomic_ops (pheromone.hpp:37-54, 366) */
-    int64_t fallbacks;     /* construction steps resolved by the exact fallback walk */
+    int64_t fallbacks;     /* construction steps resolved by the exact fallback walk
+                              (roulette tier 3; nn: full-row argmax scans + exact folds) */
     int64_t best_so_far;   /* Engine::best_length after this iteration */
+    int64_t certified_fp64; /* roulette steps the fp32 certification left open and the
+                               fp64 re-sum over the staged row certified (tier 2) */
 } aco_gpu_iter_record;
 
 /* ---- host-side model (C++ in libaco_gpu.so; no device work) ---------- */
@@ -138,6 +156,15 @@ aco_status aco_tour_length(int32_t n, const int32_t* dist, const int32_t* tour,
                            int32_t tour_len, int64_t* out);
 aco_status aco_predicted_access_cost(int32_t deposit, int32_t n, int32_t m, int32_t theta,
                                      double out[4]);
+/* Parameters::validate (model.hpp:39-53) with the engine's m = 0 -> n rule
+ * applied by the caller; nn_selected as in the reference. */
+aco_status aco_validate_parameters(double alpha, double beta, double rho, int32_t m, int32_t nn,
+                                   int32_t iterations, int32_t tile_size, int32_t n,
+                                   int32_t nn_selected);
+/* RngStream::uniform_at (rng.hpp:74-80) on the host: the draw (seed;
+ * iteration, ant, step, draw) — the same Philox4x32-10 the kernels run. */
+double aco_uniform_at(uint64_t seed, uint32_t iteration, uint32_t ant, uint32_t step,
+                      uint32_t draw);
 const char* aco_last_error(void); /* last host-side error message (thread-local) */
 
 /* ---- device engine --------------------------------------------------- */
@@ -164,6 +191,12 @@ aco_status aco_gpu_update(aco_gpu_ctx* ctx, aco_gpu_iter_record* rec);
 aco_status aco_gpu_iterate(aco_gpu_ctx* ctx, aco_gpu_iter_record* rec, int32_t* tours_out,
                            int64_t* lengths_out);
 
+/* TourBuffer::make's validation (pheromone.hpp:67-90) of caller-supplied
+ * closed tours (count rows of n+1 cities) and their stored lengths, on the
+ * device: ACO_E_NOT_CLOSED / ACO_E_NOT_A_PERMUTATION /
+ * ACO_E_INCONSISTENT_LENGTH for the first failing tour (ascending order). */
+aco_status aco_gpu_validate_tours(aco_gpu_ctx* ctx, const int32_t* tours, const int64_t* lengths,
+                                  int32_t count);
 aco_status aco_gpu_get_pheromone(aco_gpu_ctx* ctx, double* tau);
 aco_status aco_gpu_get_choice(aco_gpu_ctx* ctx, double* choice);
 /* choice32 as the construction kernel streams it, de-permuted and unscaled

@@ -18,6 +18,8 @@ ACO_OK = 0
 ACO_E_CUDA = 100
 ACO_E_NCCL = 101
 ACO_E_UNSUPPORTED = 102
+ACO_WIRE_FP64 = 0
+ACO_WIRE_FP32 = 1
 
 
 class aco_gpu_params(C.Structure):
@@ -31,6 +33,8 @@ class aco_gpu_params(C.Structure):
         ("rank", C.c_int32), ("world", C.c_int32),
         ("ant_begin", C.c_int32), ("ant_end", C.c_int32),
         ("nccl_id", C.c_uint8 * 128),
+        ("wire", C.c_int32),
+        ("validate_tours", C.c_int32),
     ]
 
 
@@ -47,6 +51,7 @@ class aco_gpu_iter_record(C.Structure):
         ("ledger", C.c_double * 4),
         ("fallbacks", C.c_int64),
         ("best_so_far", C.c_int64),
+        ("certified_fp64", C.c_int64),
     ]
 
 
@@ -54,12 +59,12 @@ class aco_gpu_iter_record(C.Structure):
 EXPORTS = [
     "aco_errc_name", "aco_parse_instance", "aco_parse_tour", "aco_build_distances",
     "aco_build_nn_lists", "aco_greedy_tour_length", "aco_tour_length",
-    "aco_predicted_access_cost", "aco_last_error", "aco_gpu_create", "aco_gpu_destroy",
+    "aco_predicted_access_cost", "aco_validate_parameters", "aco_uniform_at", "aco_last_error", "aco_gpu_create", "aco_gpu_destroy",
     "aco_gpu_last_error", "aco_gpu_set_pheromone", "aco_gpu_compute_choice_info",
     "aco_gpu_construct", "aco_gpu_update", "aco_gpu_iterate", "aco_gpu_get_pheromone",
     "aco_gpu_get_choice", "aco_gpu_get_choice32", "aco_gpu_get_topk", "aco_gpu_get_tours", "aco_gpu_get_best",
     "aco_gpu_get_info", "aco_gpu_stream", "aco_gpu_exchange_buffers", "aco_gpu_launch_count", "aco_gpu_describe", "aco_gpu_nccl_unique_id",
-    "aco_gpu_philox_uniform",
+    "aco_gpu_philox_uniform", "aco_gpu_validate_tours",
 ]
 
 _p = C.c_void_p
@@ -83,6 +88,10 @@ def _load() -> C.CDLL:
     L.aco_greedy_tour_length.argtypes = [_i32, _p, C.POINTER(C.c_int64)]
     L.aco_tour_length.argtypes = [_i32, _p, _p, _i32, C.POINTER(C.c_int64)]
     L.aco_predicted_access_cost.argtypes = [_i32, _i32, _i32, _i32, _p]
+    L.aco_validate_parameters.argtypes = [C.c_double, C.c_double, C.c_double, _i32, _i32, _i32,
+                                          _i32, _i32, _i32]
+    L.aco_uniform_at.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]
+    L.aco_uniform_at.restype = C.c_double
     L.aco_gpu_create.argtypes = [C.POINTER(aco_gpu_params), _p, C.POINTER(_p)]
     L.aco_gpu_destroy.argtypes = [_p]
     L.aco_gpu_destroy.restype = None
@@ -93,6 +102,7 @@ def _load() -> C.CDLL:
     L.aco_gpu_construct.argtypes = [_p, C.POINTER(aco_gpu_iter_record)]
     L.aco_gpu_update.argtypes = [_p, C.POINTER(aco_gpu_iter_record)]
     L.aco_gpu_iterate.argtypes = [_p, C.POINTER(aco_gpu_iter_record), _p, _p]
+    L.aco_gpu_validate_tours.argtypes = [_p, _p, _p, _i32]
     L.aco_gpu_get_pheromone.argtypes = [_p, _p]
     L.aco_gpu_get_choice.argtypes = [_p, _p]
     L.aco_gpu_get_choice32.argtypes = [_p, _p, _p]
@@ -119,5 +129,6 @@ lib = _load()
 
 
 def ptr(a: np.ndarray) -> int:
-    assert a.flags["C_CONTIGUOUS"]
+    if not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("buffers passed to libaco_gpu.so must be C-contiguous")
     return a.ctypes.data

@@ -131,13 +131,17 @@ struct aco_gpu_ctx {
     float* d_delta32 = nullptr; // sharded atomic path over NCCL: the fp32 wire copy of d_delta
     long long* d_stats = nullptr;   // [0..2] stats, [3] best_so_far
     int32_t* d_best = nullptr;      // n+1
-    unsigned long long* d_fb = nullptr; // [0] roulette fallbacks, [1] nn argmax fallbacks
+    unsigned long long* d_fb = nullptr; // [0] exact fallbacks, [1] nn argmax fallbacks, [2] roulette tier-2
     unsigned long long* d_timing = nullptr; // ACO_TIMING phase cycles
     long long* h_stats = nullptr;       // pinned: [0..7] d_stats, [8..9] fallback counters
     int32_t* d_tourbuf = nullptr;       // sharded: winning tour exchange buffer (n+1)
     ncclComm_t comm = nullptr;
     bool external = false; // world > 1 without an NCCL id: the caller exchanges
     bool sharded = false;  // the sharded protocol (world > 1, or a 1-rank NCCL communicator)
+    int key_shift = 24;         // sharded iteration-best key: (length << key_shift) | ant
+    bool key_two_stage = false; // lengths too long to pack: MIN length, then MIN ant
+    bool validate_tours = false;      // debug mode: k_validate_tours after every construction
+    unsigned long long* d_verr = nullptr;
 };
 
 namespace {
@@ -185,6 +189,12 @@ void check_launch(aco_gpu_ctx* c, const char* what) {
 }
 
 int round_up(int x, int a) { return (x + a - 1) / a * a; }
+
+// ACO_DEBUG=1 prints each construction launch shape (read once per process)
+bool debug_enabled() {
+    static const bool on = std::getenv("ACO_DEBUG") != nullptr;
+    return on;
+}
 
 __global__ void k_fill(double* p, size_t count, double v) {
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
@@ -404,6 +414,7 @@ ConstructParams make_cp(aco_gpu_ctx* c) {
     p.tours = c->d_tours;
     p.fallbacks = c->d_fb;
     p.argmax_fallbacks = c->d_fb + 1;
+    p.tier2 = c->d_fb + 2;
     p.n = c->n;
     p.P64 = c->P64;
     p.PW = c->PW;
@@ -471,7 +482,7 @@ void launch_construct(aco_gpu_ctx* c) {
                             std::to_string(c->NV) + "> grid=" + std::to_string(grid) +
                             " per_sm=" + std::to_string(per_sm) + " smem=" + std::to_string(smem) +
                             " row=" + std::to_string(c->PW);
-        if (std::getenv("ACO_DEBUG"))
+        if (debug_enabled())
             std::fprintf(stderr, "construct: %s\n", c->construct_desc.c_str());
         fn<<<grid, 32 * c->team, smem, c->stream>>>(p);
         check_launch(c, "k_construct_team");
@@ -495,7 +506,7 @@ void launch_construct(aco_gpu_ctx* c) {
                             std::to_string(grid) + " per_sm=" + std::to_string(per_sm) +
                             " smem=" + std::to_string(smem) + " row=" + std::to_string(c->PW) +
                             (st ? " streams_tours_to_host" : "");
-        if (std::getenv("ACO_DEBUG"))
+        if (debug_enabled())
             std::fprintf(stderr, "construct: %s\n", c->construct_desc.c_str());
         fn<<<grid, 32, smem, c->stream>>>(p);
         check_launch(c, "k_construct_roulette");
@@ -526,9 +537,47 @@ void launch_construct(aco_gpu_ctx* c) {
 }
 
 
+// Debug mode: validate this construction's tours on the device and fail
+// the call (before any deposit) the way TourBuffer::make would throw.
+void check_tours(aco_gpu_ctx* c, const int32_t* d_tours = nullptr, const int64_t* d_len = nullptr,
+                 int count = -1, int ant0 = -1) {
+    if (!d_tours) {
+        d_tours = c->d_tours;
+        d_len = c->d_len;
+        count = c->mloc;
+        ant0 = c->ant_begin;
+    }
+    if (count <= 0) return;
+    const unsigned long long none = ~0ull;
+    CK(cudaMemcpyAsync(c->d_verr, &none, sizeof(none), cudaMemcpyHostToDevice, c->stream));
+    const int words = (c->n + 31) / 32;
+    const size_t smem = 4 * static_cast<size_t>(words) * sizeof(uint32_t);
+    if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(k_validate_tours, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+    const int grid = std::max(1, std::min((count + 3) / 4, c->num_sms * 8));
+    k_validate_tours<<<grid, 128, smem, c->stream>>>(d_tours, c->d_dist, d_len, c->n, c->P64,
+                                                      count, c->d_verr);
+    check_launch(c, "k_validate_tours");
+    unsigned long long e = 0;
+    CK(cudaMemcpyAsync(&e, c->d_verr, sizeof(e), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (e == none) return;
+    const long long ant = ant0 + static_cast<long long>(e >> 2);
+    switch (e & 3) {
+    case 1: throw ModelError(Errc::not_closed, "tour does not return to its start (ant " +
+                                                   std::to_string(ant) + ")");
+    case 2: throw ModelError(Errc::not_a_permutation, "tour is not a permutation of 0.." +
+                                                          std::to_string(c->n - 1) + " (ant " +
+                                                          std::to_string(ant) + ")");
+    default: throw ModelError(Errc::inconsistent_length,
+                              "stored length of ant " + std::to_string(ant) + " != recomputed");
+    }
+}
+
 // construction + tour lengths + iteration stats (no host sync)
 void do_construct(aco_gpu_ctx* c) {
-    CK(cudaMemsetAsync(c->d_fb, 0, 2 * sizeof(unsigned long long), c->stream));
+    CK(cudaMemsetAsync(c->d_fb, 0, 3 * sizeof(unsigned long long), c->stream));
     CK(cudaEventRecord(c->ev[0], c->stream));
     launch_construct(c);
     CK(cudaEventRecord(c->ev[1], c->stream));
@@ -546,6 +595,7 @@ void do_construct(aco_gpu_ctx* c) {
             c->d_inv + static_cast<size_t>(c->rank) * c->S, succ, pred, c->S);
         check_launch(c, "k_tour_length");
     }
+    if (c->validate_tours) check_tours(c);
     // unsharded: the stats kernel also maintains best-so-far on device.
     k_iter_stats<<<1, 1024, 0, c->stream>>>(
         c->d_len, c->mloc, c->d_tours, c->n, c->d_stats, c->d_stats + 3, c->d_best,
@@ -618,17 +668,23 @@ float ev_ms(aco_gpu_ctx* c, int a, int b) {
 void enqueue_shard_stats(aco_gpu_ctx* c) {
     auto& api = nccl();
     long long* s = c->d_stats;
-    k_shard_key<<<1, 32, 0, c->stream>>>(s, c->ant_begin, c->mloc);
+    const int shift = c->key_two_stage ? 0 : c->key_shift;
+    k_shard_key<<<1, 32, 0, c->stream>>>(s, c->ant_begin, c->mloc, shift);
     check_launch(c, "k_shard_key");
     NK(api.GroupStart());
     NK(api.AllReduce(s + 4, s + 4, 1, ncclInt64, ncclMin, c->comm, c->stream));
     NK(api.AllReduce(s + 6, s + 6, 1, ncclInt64, ncclSum, c->comm, c->stream));
     NK(api.GroupEnd());
+    if (c->key_two_stage) { // s[5] = lowest global ant among the ranks holding min length
+        k_shard_ant<<<1, 32, 0, c->stream>>>(s, c->ant_begin, c->mloc);
+        check_launch(c, "k_shard_ant");
+        NK(api.AllReduce(s + 5, s + 5, 1, ncclInt64, ncclMin, c->comm, c->stream));
+    }
     k_owner_tour<<<std::max(1, (c->n + 256) / 256), 256, 0, c->stream>>>(
-        s, c->d_tours, c->n, c->ant_begin, c->ant_end, c->d_tourbuf);
+        s, c->d_tours, c->n, c->ant_begin, c->ant_end, c->d_tourbuf, shift);
     check_launch(c, "k_owner_tour");
     NK(api.AllReduce(c->d_tourbuf, c->d_tourbuf, c->n + 1, ncclInt32, ncclMax, c->comm, c->stream));
-    k_best_update<<<1, 1024, 0, c->stream>>>(s, c->d_tourbuf, c->n, c->d_best);
+    k_best_update<<<1, 1024, 0, c->stream>>>(s, c->d_tourbuf, c->n, c->d_best, shift);
     check_launch(c, "k_best_update");
 }
 
@@ -637,7 +693,7 @@ void enqueue_shard_stats(aco_gpu_ctx* c) {
 // otherwise (and in external mode) this shard's own statistics.
 void finish_stats(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
     if (c->sharded && !c->external) {
-        rec->best_length = c->h_stats[4] >> 24;
+        rec->best_length = c->key_two_stage ? c->h_stats[4] : c->h_stats[4] >> c->key_shift;
         rec->mean_length = static_cast<double>(c->h_stats[6]) / static_cast<double>(c->m);
         c->best_so_far = c->h_stats[3];
     } else {
@@ -722,6 +778,29 @@ aco_status aco_predicted_access_cost(int32_t deposit, int32_t n, int32_t m, int3
     });
 }
 
+aco_status aco_validate_parameters(double alpha, double beta, double rho, int32_t m, int32_t nn,
+                                   int32_t iterations, int32_t tile_size, int32_t n,
+                                   int32_t nn_selected) {
+    return guard_ctx(nullptr, [&] {
+        Config c;
+        c.n = n;
+        c.m = m;
+        c.nn = nn;
+        c.theta = tile_size;
+        c.iterations = iterations;
+        c.selection = nn_selected ? ACO_SEL_NN : ACO_SEL_ROULETTE;
+        c.alpha = alpha;
+        c.beta = beta;
+        c.rho = rho;
+        validate(c);
+    });
+}
+
+double aco_uniform_at(uint64_t seed, uint32_t iteration, uint32_t ant, uint32_t step,
+                      uint32_t draw) {
+    return philox_uniform(seed, iteration, ant, step, draw);
+}
+
 aco_status aco_gpu_nccl_unique_id(uint8_t out[128]) {
     return guard_ctx(nullptr, [&] {
         auto& api = nccl();
@@ -773,6 +852,7 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         }
         c->mloc = c->ant_end - c->ant_begin;
         c->device = prm->device;
+        c->validate_tours = prm->validate_tours != 0;
         {
             // world > 1 with a zero id: external exchange (the caller runs
             // the collectives); world == 1 with an id: the sharded protocol on
@@ -882,9 +962,10 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
             (warp_gather && !(gsplit && gsplit[0] == '0'))) {
             CK(cudaMalloc(&c->d_delta, cells * sizeof(double)));
             CK(cudaMemset(c->d_delta, 0, cells * sizeof(double)));
-            const char* wire = std::getenv("ACO_WIRE_FP64"); // "1": all-reduce the fp64 delta
+            // fp32 wire only on request (aco_gpu_params::wire): the default
+            // all-reduces the fp64 delta, so tours do not depend on G
             if (c->sharded && !c->external && c->cfg.deposit == ACO_DEP_ACCUMULATE &&
-                !(wire && wire[0] == '1'))
+                prm->wire == ACO_WIRE_FP32)
                 CK(cudaMalloc(&c->d_delta32, cells * sizeof(float)));
         }
         CK(cudaMalloc(&c->d_stats, 8 * sizeof(long long)));
@@ -892,14 +973,23 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         CK(cudaMemcpy(c->d_stats, init_stats, sizeof(init_stats), cudaMemcpyHostToDevice));
         CK(cudaMalloc(&c->d_best, (n + 1) * sizeof(int32_t)));
         CK(cudaMemset(c->d_best, 0, (n + 1) * sizeof(int32_t)));
-        CK(cudaMalloc(&c->d_fb, 2 * sizeof(unsigned long long)));
+        CK(cudaMalloc(&c->d_verr, sizeof(unsigned long long)));
+        CK(cudaMalloc(&c->d_fb, 3 * sizeof(unsigned long long)));
+        CK(cudaMemset(c->d_fb, 0, 3 * sizeof(unsigned long long)));
 #if ACO_TIMING
         CK(cudaMalloc(&c->d_timing, 8 * sizeof(unsigned long long)));
         CK(cudaMemset(c->d_timing, 0, 8 * sizeof(unsigned long long)));
 #endif
         CK(cudaMallocHost(&c->h_stats, 16 * sizeof(long long)));
         if (c->sharded) {
-            if (c->m >= (1 << 24)) throw Fail{ACO_E_UNSUPPORTED, "sharded colonies support m < 2^24 ants"};
+            // iteration-best key: (length << key_shift) | global ant in ONE
+            // MIN all-reduce when every tour length fits (length < n * max_d);
+            // otherwise two MIN all-reduces, the length and then the lowest
+            // ant among the ranks that hold it (engine.hpp:117-129 tie rule)
+            c->key_shift = 1;
+            while ((int64_t{1} << c->key_shift) < c->m) ++c->key_shift;
+            const int64_t max_len = static_cast<int64_t>(n) * std::max<int64_t>(c->max_d, 1);
+            c->key_two_stage = c->key_shift >= 62 || max_len >= (int64_t{1} << (62 - c->key_shift));
             CK(cudaMalloc(&c->d_tourbuf, (n + 1) * sizeof(int32_t)));
         }
 
@@ -948,7 +1038,7 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
     if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
     void* bufs[] = {c->d_choice_nn, c->d_choice_nn32, c->d_nn_scale, c->d_topk, c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
                     c->d_choice_p64, c->d_scale, c->d_nn, c->d_tours, c->d_len, c->d_inv,
-                    c->d_succ, c->d_pred, c->d_delta, c->d_delta32, c->d_stats, c->d_best, c->d_fb, c->d_tourbuf};
+                    c->d_succ, c->d_pred, c->d_delta, c->d_delta32, c->d_stats, c->d_best, c->d_fb, c->d_tourbuf, c->d_verr};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_stats) cudaFreeHost(c->h_stats);
@@ -1015,7 +1105,7 @@ aco_status aco_gpu_construct(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
         do_construct(c);
         if (c->sharded && !c->external) enqueue_shard_stats(c);
         CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 8 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(c->h_stats + 8, c->d_fb, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h_stats + 8, c->d_fb, 3 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         aco_gpu_iter_record tmp{};
         aco_gpu_iter_record* r = rec ? rec : &tmp;
@@ -1027,6 +1117,7 @@ aco_status aco_gpu_construct(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
         r->construct_ms = ev_ms(c, 0, 2);
         r->construct_kernel_ms = ev_ms(c, 0, 1);
         r->fallbacks = fb0 + fb1;
+        r->certified_fp64 = c->h_stats[10];
         r->best_so_far = c->best_so_far;
     });
 }
@@ -1084,7 +1175,7 @@ aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* to
         }
         do_update(c);
         CK(cudaMemcpyAsync(c->h_stats, c->d_stats, 8 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(c->h_stats + 8, c->d_fb, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h_stats + 8, c->d_fb, 3 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         if (tours_out || lengths_out) CK(cudaStreamSynchronize(c->copy_stream));
         finish_stats(c, r);
@@ -1094,10 +1185,34 @@ aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* to
         r->exchange_ms = ev_ms(c, 2, 3);
         r->choice_ms = (!gather_mode(c) && !c->sharded) ? ev_ms(c, 4, 5) : 0.0;
         r->fallbacks = c->h_stats[8] + c->h_stats[9];
+        r->certified_fp64 = c->h_stats[10];
         c->last_fb[0] = c->h_stats[8];
         c->last_fb[1] = c->h_stats[9];
         r->best_so_far = c->best_so_far;
         ++c->iteration;
+    });
+}
+
+aco_status aco_gpu_validate_tours(aco_gpu_ctx* c, const int32_t* tours, const int64_t* lengths,
+                                  int32_t count) {
+    return guard_ctx(c, [&] {
+        if (count < 0 || (count > 0 && (!tours || !lengths)))
+            throw ModelError(Errc::config_error, "tours and lengths are required");
+        if (count == 0) return;
+        CK(cudaSetDevice(c->device));
+        int32_t* dt = nullptr;
+        int64_t* dl = nullptr;
+        const size_t tb = static_cast<size_t>(count) * (c->n + 1) * sizeof(int32_t);
+        CK(cudaMalloc(&dt, tb));
+        CK(cudaMalloc(&dl, count * sizeof(int64_t)));
+        struct Free {
+            void* a;
+            void* b;
+            ~Free() { cudaFree(a); cudaFree(b); }
+        } guard{dt, dl};
+        CK(cudaMemcpyAsync(dt, tours, tb, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(dl, lengths, count * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+        check_tours(c, dt, dl, count, 0);
     });
 }
 

@@ -102,6 +102,7 @@ struct ConstructParams {
     int32_t* tours;          // mloc x (n+1)
     unsigned long long* fallbacks;
     unsigned long long* argmax_fallbacks;
+    unsigned long long* tier2; // roulette: steps certified by the fp64 re-sum (tier 2)
     int n, P64, PW, R, nn;
     int ant_begin, mloc;
     int random_start;
@@ -592,7 +593,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
         TourStream hs{0}; // STREAM: the caller's pinned tours_out is mapped
         if constexpr (STREAM) hs.put(p, kl, 0, start, lane);
         int cur = start;
-        unsigned long long fb = 0;
+        unsigned long long fb = 0, fb2 = 0;
         bool prefetched = false; // row of `cur` already requested by the previous step
         double ubatch = 0.0;
 #if ACO_TIMING
@@ -908,6 +909,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                 if (j2 >= 0) {
                     ok = true;
                     next = j2;
+                    ++fb2;
                 }
             }
             if (!ok) {
@@ -943,6 +945,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
         if (lane == 0) {
             tour[n] = start;
             if (fb) atomicAdd(p.fallbacks, fb);
+            if (fb2) atomicAdd(p.tier2, fb2);
         }
         if constexpr (STREAM) {
             hs.put(p, kl, n, start, lane);

@@ -291,6 +291,7 @@ void validate(const Config& c) {
     if (c.alpha < 0.0 || c.beta < 0.0)
         throw ModelError(Errc::config_error, "alpha and beta must be >= 0");
     if (c.m < 0) throw ModelError(Errc::config_error, "ant count must be >= 1");
+    if (c.iterations < 1) throw ModelError(Errc::config_error, "iterations must be >= 1");
     if (c.theta < 1) throw ModelError(Errc::config_error, "tile size must be >= 1");
     if (c.selection < 0 || c.selection > 2)
         throw ModelError(Errc::config_error, "unknown selection strategy");

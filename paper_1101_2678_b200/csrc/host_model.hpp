@@ -29,7 +29,7 @@ struct Instance {
 };
 
 struct Config {
-    int n = 0, m = 0, nn = 30, theta = 64, selection = 0, deposit = 0;
+    int n = 0, m = 0, nn = 30, theta = 64, selection = 0, deposit = 0, iterations = 1;
     double alpha = 1.0, beta = 2.0, rho = 0.5;
 };
 

@@ -78,6 +78,53 @@ __global__ void k_tour_length(const int32_t* __restrict__ tours, const int32_t* 
     }
 }
 
+// Debug-mode tour validation (aco_gpu_params::validate_tours): the checks
+// the reference makes on every tour before depositing — TourBuffer::make
+// (pheromone.hpp:67-90) recomputes tour_length (model.hpp:205-226), which
+// throws not_closed if tour[n] != tour[0], not_a_permutation if a city is
+// out of range or repeated, and the buffer then throws inconsistent_length if
+// the stored length differs.  One warp per ant with the ant's visited bitset
+// in shared memory; the first failure in (ant, check) order wins, as the
+// reference's ascending ant loop throws at the first one:
+// err = min over failing ants of (ant << 2) | code, code 1 not_closed,
+// 2 not_a_permutation, 3 inconsistent_length.
+__global__ void k_validate_tours(const int32_t* __restrict__ tours, const int32_t* __restrict__ dist,
+                                 const int64_t* __restrict__ len, int n, int P64, int mloc,
+                                 unsigned long long* __restrict__ err) {
+    extern __shared__ uint32_t seen_all[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int words = (n + 31) >> 5;
+    uint32_t* seen = seen_all + wib * words;
+    const int warps = blockDim.x >> 5;
+    for (int kl = blockIdx.x * warps + wib; kl < mloc; kl += gridDim.x * warps) {
+        const int32_t* t = tours + static_cast<size_t>(kl) * (n + 1);
+        for (int w = lane; w < words; w += 32) seen[w] = 0u;
+        __syncwarp();
+        unsigned long long code = 0;
+        if (t[n] != t[0]) code = 1;
+        bool dup = false;
+        long long acc = 0;
+        for (int s = lane; s < n; s += 32) {
+            const int c = t[s];
+            if (c < 0 || c >= n) {
+                dup = true;
+                continue;
+            }
+            const uint32_t bit = 1u << (c & 31);
+            if (atomicOr(seen + (c >> 5), bit) & bit) dup = true;
+            const int d = t[s + 1];
+            if (d >= 0 && d < n) acc += __ldg(dist + static_cast<size_t>(c) * P64 + d);
+        }
+        dup = __any_sync(kFull, dup);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);
+        if (code == 0 && dup) code = 2;
+        if (code == 0 && acc != len[kl]) code = 3;
+        if (lane == 0 && code) atomicMin(err, (static_cast<unsigned long long>(kl) << 2) | code);
+        __syncwarp();
+    }
+}
+
 // One CTA.  stats[0] = best length, stats[1] = best local ant, stats[2] =
 // length sum.  Copies the best tour when it strictly improves best_so_far.
 __global__ void __launch_bounds__(1024) k_iter_stats(const int64_t* __restrict__ len, int mloc,
@@ -137,32 +184,50 @@ __global__ void __launch_bounds__(1024) k_iter_stats(const int64_t* __restrict__
 
 // Sharded statistics entirely on the device (no host round trip between
 // the construction and the update).  Stage 1, before the MIN / SUM
-// all-reduces: key = (best length << 24) | global ant, so the MIN gives the
-// iteration best AND its lowest global ant (engine.hpp:117-129 tie rule).
-__global__ void k_shard_key(long long* stats, int ant_begin, int mloc) {
+// all-reduces: with shift > 0, key = (best length << shift) | global ant, so
+// the MIN gives the iteration best AND its lowest global ant (engine.hpp:
+// 117-129 tie rule) in one collective — the host picks shift so that every
+// possible length fits (n * max_d < 2^(62 - shift)); with shift == 0 the key
+// is the length alone and k_shard_ant + a second MIN resolve the ant.
+__global__ void k_shard_key(long long* stats, int ant_begin, int mloc, int shift) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
-        stats[4] = mloc > 0 ? (stats[0] << 24) | static_cast<long long>(ant_begin + stats[1])
-                            : LLONG_MAX;
+        stats[4] = mloc <= 0 ? LLONG_MAX
+                   : shift > 0 ? (stats[0] << shift) | static_cast<long long>(ant_begin + stats[1])
+                               : stats[0];
         stats[6] = stats[2];
     }
+}
+// Two-stage key, after the length MIN: this rank's candidate ant if its own
+// best equals the global best, else +inf (then all-reduce MIN).
+__global__ void k_shard_ant(long long* stats, int ant_begin, int mloc) {
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+        stats[5] = (mloc > 0 && stats[0] == stats[4]) ? static_cast<long long>(ant_begin + stats[1])
+                                                      : LLONG_MAX;
+}
+__device__ __forceinline__ long long shard_best_len(const long long* stats, int shift) {
+    return shift > 0 ? stats[4] >> shift : stats[4];
+}
+__device__ __forceinline__ long long shard_best_ant(const long long* stats, int shift) {
+    if (stats[4] == LLONG_MAX) return -1;
+    return shift > 0 ? (stats[4] & ((1LL << shift) - 1)) : stats[5];
 }
 // Stage 2, after them: the rank owning the winning ant copies its tour into
 // the exchange buffer, the others zero it; an all-reduce MAX replicates it
 // (tour entries are >= 0).
 __global__ void k_owner_tour(const long long* __restrict__ stats, const int32_t* __restrict__ tours,
-                             int n, int ant_begin, int ant_end, int32_t* __restrict__ tourbuf) {
-    const long long key = stats[4];
-    const int ant = static_cast<int>(key & 0xFFFFFF);
-    const bool own = key != LLONG_MAX && ant >= ant_begin && ant < ant_end;
+                             int n, int ant_begin, int ant_end, int32_t* __restrict__ tourbuf,
+                             int shift) {
+    const long long ant = shard_best_ant(stats, shift);
+    const bool own = ant >= ant_begin && ant < ant_end;
     const int32_t* src = tours + static_cast<size_t>(own ? ant - ant_begin : 0) * (n + 1);
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s <= n; s += gridDim.x * blockDim.x)
         tourbuf[s] = own ? src[s] : 0;
 }
 // Stage 3: best-so-far and its tour on strict improvement (engine.hpp:151-154).
 __global__ void __launch_bounds__(1024) k_best_update(long long* stats, const int32_t* __restrict__ tourbuf,
-                                                      int n, int32_t* __restrict__ best_tour) {
+                                                      int n, int32_t* __restrict__ best_tour, int shift) {
     __shared__ int imp;
-    const long long gl = stats[4] >> 24;
+    const long long gl = shard_best_len(stats, shift);
     if (threadIdx.x == 0) imp = gl < stats[3];
     __syncthreads();
     if (imp)

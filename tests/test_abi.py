@@ -178,3 +178,39 @@ def test_no_cpu_fallback_without_gpu(aco):
     with pytest.raises(aco.Error) as ei:
         aco.Engine(prob, aco.RunConfig())
     assert ei.value.code == 100  # ACO_E_CUDA: fails loudly, never computes on the host
+
+
+def test_host_uniform_at_matches_oracle(oracle, golden):
+    from paper_1101_2678_b200 import _lib
+
+    for seed, it, ant, st, dr, val in golden["uniform_at"][:8]:
+        assert _lib.lib.aco_uniform_at(seed, it, ant, st, dr) == float(val)
+    rng = np.random.default_rng(11)
+    for _ in range(500):
+        seed = int(rng.integers(0, 2**63))
+        args = [int(x) for x in rng.integers(0, 2**32, 4)]
+        assert _lib.lib.aco_uniform_at(seed, *args) == oracle.uniform_at(seed, *args)
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(rho=0.0), "rho must be in (0,1]"), (dict(rho=1.5), "rho must be in (0,1]"),
+    (dict(alpha=-1.0), "alpha and beta must be >= 0"), (dict(m=-1), "ant count must be >= 1"),
+    (dict(iterations=0), "iterations must be >= 1"), (dict(tile_size=0), "tile size must be >= 1"),
+    (dict(nn=10, nn_selected=1), "nn must satisfy 1 <= nn < n (n=10)"),
+])
+def test_validate_parameters_reference_messages(kw, msg):
+    """Parameters::validate (model.hpp:39-53): same checks, order and text."""
+    from paper_1101_2678_b200 import _lib
+
+    a = dict(alpha=1.0, beta=2.0, rho=0.5, m=0, nn=30, iterations=10, tile_size=64, n=10,
+             nn_selected=0)
+    a.update(kw)
+    st = _lib.lib.aco_validate_parameters(a["alpha"], a["beta"], a["rho"], a["m"], a["nn"],
+                                          a["iterations"], a["tile_size"], a["n"],
+                                          a["nn_selected"])
+    assert st == 13  # 1 + Errc::config_error
+    assert _lib.lib.aco_last_error().decode() == msg
+    a.update(rho=0.5, alpha=1.0, m=0, iterations=10, tile_size=64, nn=5)
+    assert _lib.lib.aco_validate_parameters(a["alpha"], a["beta"], a["rho"], a["m"], a["nn"],
+                                            a["iterations"], a["tile_size"], a["n"],
+                                            a["nn_selected"]) == 0

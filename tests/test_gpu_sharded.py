@@ -91,13 +91,17 @@ def test_virtual_shards_match_single_context(deposit, G, m):
         e.close()
 
 
-@pytest.mark.parametrize("deposit", [1, 0])
-def test_nccl_exchange_path_one_rank(deposit):
+@pytest.mark.parametrize("deposit,wire", [(1, 0), (0, 0), (0, 1)])
+def test_nccl_exchange_path_one_rank(deposit, wire):
     """The NCCL exchange path (all-gather of succ/pred/1/C_k, or all-reduce of
-    the local delta + k_rows<DELTA>; NCCL reduction of the statistics and
-    broadcast of the best tour) on a one-rank communicator: tours, best
+    the local delta + k_rows<DELTA/DELTA32>; NCCL reduction of the statistics
+    and broadcast of the best tour) on a one-rank communicator: tours, best
     tour and statistics equal the unsharded engine's; tau bit-exact on the
-    gather path and within 1e-5 relative on the atomic path."""
+    gather path.  Accumulate over the default fp64 wire: a free-running
+    multi-iteration trajectory (no pheromone reset) stays on the unsharded
+    colony's tours with tau within 1e-12 relative (the two differ only in the
+    order of the fp64 adds).  The opt-in fp32 wire rounds every delta once
+    (<= 1e-5 relative per iteration), so its trajectory is resynchronised."""
     from paper_1101_2678_b200 import aco
 
     n = 300
@@ -106,11 +110,12 @@ def test_nccl_exchange_path_one_rank(deposit):
     def cfg(nccl_id=None):
         return aco.RunConfig(params=aco.Parameters(m=0, seed=2),
                              selection=aco.SelectionStrategy(aco.Selection.roulette_full),
-                             deposit=aco.DepositStrategy(aco.Deposit(deposit)), nccl_id=nccl_id)
+                             deposit=aco.DepositStrategy(aco.Deposit(deposit)), nccl_id=nccl_id,
+                             wire=aco.Wire(wire))
 
     plain = aco.Engine(prob, cfg())
     nccl = aco.Engine(prob, cfg(aco.nccl_unique_id()))
-    for it in range(4):
+    for it in range(6):
         ra = plain.run_iteration()
         rb = nccl.run_iteration()
         ta, la = plain.ants()
@@ -122,8 +127,10 @@ def test_nccl_exchange_path_one_rank(deposit):
         pa, pb = plain.pheromone(), nccl.pheromone()
         if deposit != 0:
             assert np.array_equal(pa, pb)
+        elif wire == 0:
+            assert (np.abs(pa - pb) / pa).max() <= 1e-12
         else:
             assert (np.abs(pa - pb) / pa).max() <= 1e-5
-            nccl.set_pheromone(pa)  # keep the construction inputs identical
+            nccl.set_pheromone(pa)  # fp32 wire: keep the construction inputs identical
     plain.close()
     nccl.close()

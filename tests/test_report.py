@@ -64,29 +64,3 @@ def test_report_json_and_csv_match_reference(report, deposit):
     assert len(rows_m) == len(rows_r)
     for a, b in zip(rows_m, rows_r):
         assert a[:7] + a[9:] == b[:7] + b[9:]  # all but the two timing columns
-
-
-def test_cli_io_error_exit_code(tmp_path):
-    from paper_1101_2678_b200.__main__ import main
-
-    assert main(["solve", str(tmp_path / "missing.tsp")]) == 2
-    bad = tmp_path / "bad.tsp"
-    bad.write_text("NAME: x\nDIMENSION: 3\n")
-    assert main(["solve", str(bad)]) == 2
-
-
-@pytest.mark.gpu
-def test_cli_solve_verify_att48(tmp_path, golden):
-    from paper_1101_2678_b200.__main__ import main
-
-    g = golden["att48"]
-    text = "NAME : att48\nTYPE : TSP\nDIMENSION : 48\nEDGE_WEIGHT_TYPE : ATT\nNODE_COORD_SECTION\n" + \
-        "".join(f"{i + 1} {x:g} {y:g}\n" for i, (x, y) in enumerate(zip(g["xs"], g["ys"]))) + "EOF\n"
-    inst = tmp_path / "att48.tsp"
-    inst.write_text(text)
-    out = tmp_path / "r.json"
-    assert main(["solve", str(inst), "--selection", "roulette", "--iters", "10",
-                 "--out", str(out)]) == 0
-    rep = json.loads(out.read_text())
-    assert [r["best_len"] for r in rep["per_iteration"]] == g["trace_roulette_accumulate"]["best"]
-    assert main(["verify", str(inst), "--selection", "roulette"]) == 0
