@@ -235,6 +235,13 @@ int64_t aco_gpu_launch_count(const aco_gpu_ctx* ctx);
 /* NCCL unique id for world > 1 (rank 0 creates it, the caller distributes it). */
 aco_status aco_gpu_nccl_unique_id(uint8_t out[128]);
 
+/* The device replay of the host libm's pow (pow(tau, alpha) in choice_info
+ * for alpha not in {0, 1}, model.hpp:167), for unit parity tests:
+ * out[i] = pow(xs[i], ys[i]) for xs >= +0 finite, ys > 0 finite.
+ * ACO_E_UNSUPPORTED when the host libm's pow tables cannot be located. */
+aco_status aco_gpu_libm_pow(int32_t device, int32_t count, const double* xs, const double* ys,
+                            double* out);
+
 /* Device self-test helpers (unit parity of the device RNG / scan pieces). */
 aco_status aco_gpu_philox_uniform(int32_t device, uint64_t seed, uint32_t iteration,
                                   uint32_t ant, int32_t count, const uint32_t* steps,

@@ -363,3 +363,9 @@ void orc_update(int n, int m, const int32_t* tours, const int64_t* lengths, doub
     for (size_t c = 0; c < cells; ++c) tau[c] += acc[c];            /* :220 */
     free(acc);
 }
+
+/* The host libm's pow over arrays (the function model.hpp:167 calls), for
+ * the device libm_pow parity test. */
+void orc_pow(int n, const double* x, const double* y, double* out) {
+    for (int i = 0; i < n; ++i) out[i] = pow(x[i], y[i]);
+}

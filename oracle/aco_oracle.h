@@ -30,6 +30,7 @@ double orc_tau0(int n, const int32_t* dist, int m);
 int orc_build_nn_lists(int n, const int32_t* dist, int nn, int32_t* out);
 void orc_choice_info(int n, const int32_t* dist, const double* tau, double alpha, double beta,
                      double* choice);
+void orc_pow(int n, const double* x, const double* y, double* out);
 int64_t orc_tour_length(int n, const int32_t* dist, const int32_t* tour);
 
 /* selection: 0 roulette_full, 1 roulette_nn, 2 data_parallel_tiled */

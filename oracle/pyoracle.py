@@ -82,6 +82,7 @@ class Oracle:
                                     C.c_uint64, C.c_uint32, C.c_int, C.c_int, C.c_int, _i32p,
                                     _i64p, _i64p]
         L.orc_update.argtypes = [C.c_int, C.c_int, _i32p, _i64p, C.c_double, C.c_int, _f64p]
+        L.orc_pow.argtypes = [C.c_int, _f64p, _f64p, _f64p]
 
     # -- rng.hpp
     def philox(self, ctr, key):
@@ -120,6 +121,13 @@ class Oracle:
         n = dist.shape[0]
         out = np.zeros((n, n), np.float64)
         self.lib.orc_choice_info(n, dist, np.ascontiguousarray(tau), alpha, beta, out)
+        return out
+
+    def pow(self, x, y):
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.ascontiguousarray(np.broadcast_to(y, x.shape), np.float64)
+        out = np.zeros_like(x)
+        self.lib.orc_pow(len(x), x, y, out)
         return out
 
     def tour_length(self, dist, tour):

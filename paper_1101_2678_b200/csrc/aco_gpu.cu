@@ -135,6 +135,7 @@ struct aco_gpu_ctx {
     unsigned long long* d_timing = nullptr; // ACO_TIMING phase cycles
     long long* h_stats = nullptr;       // pinned: [0..7] d_stats, [8..9] fallback counters
     int32_t* d_tourbuf = nullptr;       // sharded: winning tour exchange buffer (n+1)
+    LibmPowTables* d_powtab = nullptr;  // alpha not in {0, 1}: the host libm's pow tables
     ncclComm_t comm = nullptr;
     bool external = false; // world > 1 without an NCCL id: the caller exchanges
     bool sharded = false;  // the sharded protocol (world > 1, or a 1-rank NCCL communicator)
@@ -357,6 +358,7 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
     rp.m = !c->sharded ? c->mloc : c->m; // a local ant range is one shard of mloc ants
     rp.alpha = c->cfg.alpha;
     rp.keep = 1.0 - c->cfg.rho; // pheromone.hpp:179
+    rp.powtab = c->d_powtab;
     const size_t smem = static_cast<size_t>(c->P64) * sizeof(double);
     const size_t wsmem = smem + 64 * sizeof(double);
     if (mode == MODE_GATHER && wsmem <= 32 * 1024) { // one warp per row
@@ -536,6 +538,75 @@ void launch_construct(aco_gpu_ctx* c) {
     }
 }
 
+
+// pow(tau, alpha) for alpha not in {0, 1}: upload the host libm's pow tables
+// and prove on this device that libm_pow replays the host's std::pow on a
+// spread of pheromone-like arguments (tau0-scaled, down through the
+// subnormals, plus random mantissas) — otherwise refuse (ACO_E_UNSUPPORTED),
+// never run a silently different pow.
+LibmPowTables* upload_pow_tables(cudaStream_t st) {
+    LibmPowTables T;
+    std::string why;
+    if (!read_libm_pow_tables(T, why))
+        throw Fail{ACO_E_UNSUPPORTED, "pow(tau, alpha) for alpha not in {0,1}: " + why};
+    LibmPowTables* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(T)));
+    CK(cudaMemcpyAsync(d, &T, sizeof(T), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return d;
+}
+
+void pow_self_test(const LibmPowTables* d_tab, double alpha, double tau0, cudaStream_t st) {
+    std::vector<double> xs, ys;
+    uint64_t s = 0x9E3779B97F4A7C15ull;
+    auto next = [&] {
+        s ^= s << 13;
+        s ^= s >> 7;
+        s ^= s << 17;
+        return s;
+    };
+    for (int e = -1100; e <= 40; ++e) { // tau0 * 2^e and random neighbours
+        xs.push_back(std::ldexp(tau0, e));
+        const double m = 1.0 + static_cast<double>(next() >> 11) * 0x1.0p-53;
+        xs.push_back(std::ldexp(m, e));
+    }
+    for (int k = 0; k < 2048; ++k) {
+        const uint64_t bits = (next() & 0x000FFFFFFFFFFFFFull) | (static_cast<uint64_t>(next() % 0x7FE) << 52);
+        double x;
+        std::memcpy(&x, &bits, 8);
+        xs.push_back(x);
+    }
+    xs.push_back(0.0);
+    xs.push_back(1.0);
+    ys.assign(xs.size(), alpha);
+    const int cnt = static_cast<int>(xs.size());
+    double *dx = nullptr, *dy = nullptr, *dout = nullptr;
+    CK(cudaMalloc(&dx, cnt * sizeof(double)));
+    CK(cudaMalloc(&dy, cnt * sizeof(double)));
+    CK(cudaMalloc(&dout, cnt * sizeof(double)));
+    std::vector<double> out(cnt);
+    CK(cudaMemcpyAsync(dx, xs.data(), cnt * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dy, ys.data(), cnt * sizeof(double), cudaMemcpyHostToDevice, st));
+    k_libm_pow<<<(cnt + 255) / 256, 256, 0, st>>>(dx, dy, cnt, d_tab, dout);
+    const cudaError_t le = cudaGetLastError();
+    CK(cudaMemcpyAsync(out.data(), dout, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    cudaFree(dx);
+    cudaFree(dy);
+    cudaFree(dout);
+    if (le != cudaSuccess) throw Fail{ACO_E_CUDA, std::string("k_libm_pow: ") + cudaGetErrorString(le)};
+    for (int i = 0; i < cnt; ++i) {
+        const double h = host_pow(xs[i], ys[i]);
+        if (std::memcmp(&h, &out[i], 8) != 0) {
+            char buf[160];
+            std::snprintf(buf, sizeof(buf), "device pow(%a, %a) = %a but host libm gives %a", xs[i],
+                          ys[i], out[i], h);
+            throw Fail{ACO_E_UNSUPPORTED,
+                       std::string("pow(tau, alpha) for alpha not in {0,1} cannot be reproduced "
+                                   "on this host: ") + buf};
+        }
+    }
+}
 
 // Debug mode: validate this construction's tours on the device and fail
 // the call (before any deposit) the way TourBuffer::make would throw.
@@ -1001,6 +1072,11 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
             NK(api.CommInitRank(&c->comm, c->world, id, c->rank));
         }
 
+        if (c->cfg.alpha != 0.0 && c->cfg.alpha != 1.0) {
+            c->d_powtab = upload_pow_tables(c->stream);
+            pow_self_test(c->d_powtab, c->cfg.alpha, c->tau0, c->stream);
+        }
+
         // tau0 everywhere (diagonal included, model.hpp:258-262), then choice
         k_fill<<<c->num_sms * 4, 256, 0, c->stream>>>(c->d_tau, cells, c->tau0);
         check_launch(c, "k_fill");
@@ -1038,7 +1114,7 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
     if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
     void* bufs[] = {c->d_choice_nn, c->d_choice_nn32, c->d_nn_scale, c->d_topk, c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
                     c->d_choice_p64, c->d_scale, c->d_nn, c->d_tours, c->d_len, c->d_inv,
-                    c->d_succ, c->d_pred, c->d_delta, c->d_delta32, c->d_stats, c->d_best, c->d_fb, c->d_tourbuf, c->d_verr};
+                    c->d_succ, c->d_pred, c->d_delta, c->d_delta32, c->d_stats, c->d_best, c->d_fb, c->d_tourbuf, c->d_verr, c->d_powtab};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_stats) cudaFreeHost(c->h_stats);
@@ -1294,6 +1370,27 @@ aco_status aco_gpu_get_info(aco_gpu_ctx* c, int32_t* m, int32_t* ant_begin, int3
     if (stream) *stream = c->stream_kind;
     if (iteration) *iteration = c->iteration;
     return ACO_OK;
+}
+
+aco_status aco_gpu_libm_pow(int32_t device, int32_t count, const double* xs, const double* ys,
+                            double* out) {
+    return guard_ctx(nullptr, [&] {
+        CK(cudaSetDevice(device));
+        LibmPowTables* tab = upload_pow_tables(nullptr);
+        double *dx = nullptr, *dy = nullptr, *dout = nullptr;
+        CK(cudaMalloc(&dx, count * sizeof(double)));
+        CK(cudaMalloc(&dy, count * sizeof(double)));
+        CK(cudaMalloc(&dout, count * sizeof(double)));
+        CK(cudaMemcpy(dx, xs, count * sizeof(double), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dy, ys, count * sizeof(double), cudaMemcpyHostToDevice));
+        k_libm_pow<<<std::max(1, std::min((count + 255) / 256, 4096)), 256>>>(dx, dy, count, tab, dout);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(out, dout, count * sizeof(double), cudaMemcpyDeviceToHost));
+        cudaFree(dx);
+        cudaFree(dy);
+        cudaFree(dout);
+        cudaFree(tab);
+    });
 }
 
 aco_status aco_gpu_philox_uniform(int32_t device, uint64_t seed, uint32_t it, uint32_t ant,

@@ -14,6 +14,13 @@
 // exactly like the reference build (CMakeLists.txt:1-22).
 #include "host_model.hpp"
 
+#include <dlfcn.h>
+#include <link.h>
+
+#include <cstring>
+#include <fstream>
+#include <iterator>
+
 #include <algorithm>
 #include <cerrno>
 #include <charconv>
@@ -343,6 +350,95 @@ void predicted_access_cost(int deposit, int n, int m, int theta, double out[4]) 
         break;
     }
     }
+}
+
+double host_pow(double x, double y) { return std::pow(x, y); }
+
+namespace {
+
+int find_libm(struct dl_phdr_info* info, size_t, void* data) {
+    const char* name = info->dlpi_name;
+    if (name && std::strstr(name, "libm.so")) {
+        *static_cast<std::string*>(data) = name;
+        return 1;
+    }
+    return 0;
+}
+
+double rd(const std::string& img, size_t off) {
+    double v;
+    std::memcpy(&v, img.data() + off, sizeof(v));
+    return v;
+}
+
+uint64_t ru(const std::string& img, size_t off) {
+    uint64_t v;
+    std::memcpy(&v, img.data() + off, sizeof(v));
+    return v;
+}
+
+// first offset >= from where the 16 bytes (a, b) occur, or npos
+size_t find_pair(const std::string& img, double a, double b, size_t from) {
+    char pat[16];
+    std::memcpy(pat, &a, 8);
+    std::memcpy(pat + 8, &b, 8);
+    return img.find(std::string(pat, 16), from);
+}
+
+} // namespace
+
+bool read_libm_pow_tables(LibmPowTables& T, std::string& why) {
+    std::string path;
+    host_pow(2.0, 0.5); // make sure libm is mapped
+    dl_iterate_phdr(find_libm, &path);
+    if (path.empty()) {
+        why = "libm.so is not loaded";
+        return false;
+    }
+    std::ifstream f(path, std::ios::binary);
+    const std::string img((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    if (img.empty()) {
+        why = "cannot read " + path;
+        return false;
+    }
+    // __pow_log_data: {ln2hi, ln2lo} then A[0] = -0.5, then the table whose
+    // first entry is invc = 0x1.6ap+0 with a zero pad (glibc pow_log_data.c);
+    // __log_data shares the (ln2hi, ln2lo) prefix, hence the extra checks.
+    const double ln2hi = 0x1.62e42fefa3800p-1, ln2lo = 0x1.ef35793c76730p-45;
+    size_t lo = std::string::npos;
+    for (size_t at = find_pair(img, ln2hi, ln2lo, 0); at != std::string::npos;
+         at = find_pair(img, ln2hi, ln2lo, at + 1)) {
+        if (at + 72 + 128 * 32 <= img.size() && rd(img, at + 16) == -0.5 &&
+            rd(img, at + 72) == 0x1.6ap+0 && ru(img, at + 80) == 0) {
+            lo = at;
+            break;
+        }
+    }
+    // __exp_data: {InvLn2N = 0x1.71547652b82fep0 * 128, Shift = 0x1.8p52};
+    // its 2^(i/128) table starts {tail 0, sbits(1.0)} a fixed distance later
+    const size_t ex = find_pair(img, 0x1.71547652b82fep7, 0x1.8p52, 0);
+    size_t et = std::string::npos;
+    if (ex != std::string::npos)
+        for (size_t off = ex + 64; off + 16 <= img.size() && off < ex + 512; off += 8)
+            if (ru(img, off) == 0 && ru(img, off + 8) == 0x3ff0000000000000ull) {
+                et = off;
+                break;
+            }
+    if (lo == std::string::npos || et == std::string::npos || et + 256 * 8 > img.size()) {
+        why = "pow tables not found in " + path;
+        return false;
+    }
+    T.ln2hi = rd(img, lo);
+    T.ln2lo = rd(img, lo + 8);
+    for (int k = 0; k < 7; ++k) T.A[k] = rd(img, lo + 16 + 8 * k);
+    for (int k = 0; k < 128 * 4; ++k) T.ltab[k] = rd(img, lo + 72 + 8 * k);
+    T.invln2N = rd(img, ex);
+    T.shift = rd(img, ex + 8);
+    T.negln2hiN = rd(img, ex + 16);
+    T.negln2loN = rd(img, ex + 24);
+    for (int k = 0; k < 4; ++k) T.C[k] = rd(img, ex + 32 + 8 * k);
+    for (int k = 0; k < 256; ++k) T.etab[k] = ru(img, et + 8 * k);
+    return true;
 }
 
 } // namespace acob200

@@ -42,6 +42,22 @@ int64_t greedy_tour_length(int n, const int32_t* dist);
 int64_t tour_length(int n, const int32_t* dist, const int32_t* tour, int len);
 void validate(const Config& c);
 std::vector<double> eta_beta_table(int64_t max_d, double beta);
+
+// The tables of the host libm's pow (glibc __pow_log_data / __exp_data), read
+// out of the loaded libm.so so the device can replay pow(tau, alpha) exactly
+// (libm_pow.cuh).  Layout as the FMA build of glibc 2.28+ reads them.
+struct LibmPowTables {
+    // __pow_log_data: ln2hi, ln2lo, A[0..6], tab[128] = {invc, pad, logc, logctail}
+    double ln2hi, ln2lo, A[7];
+    double ltab[128 * 4];
+    // __exp_data: InvLn2N, Shift, NegLn2hiN, NegLn2loN, C2..C5, tab[2*128] = {tail, sbits}
+    double invln2N, shift, negln2hiN, negln2loN, C[4];
+    uint64_t etab[256];
+};
+// false (with the reason) when the loaded libm does not carry them
+bool read_libm_pow_tables(LibmPowTables& out, std::string& why);
+// the host libm's own pow (what compute_choice_info calls, model.hpp:167)
+double host_pow(double x, double y);
 void predicted_access_cost(int deposit, int n, int m, int theta, double out[4]);
 
 } // namespace acob200

@@ -32,6 +32,7 @@
 #include <cstdint>
 
 #include "construct.cuh"
+#include "libm_pow.cuh"
 
 namespace acob200 {
 
@@ -304,6 +305,7 @@ struct RowParams {
     int n, P64, PW, C, V, LA;
     int shards, S, m;        // ants: shard g holds global ants [g*S, min(m,(g+1)*S))
     double alpha, keep;
+    const LibmPowTables* powtab; // host libm's pow tables (alpha not in {0, 1})
 };
 
 // Write one row of the permuted streamed layout (stream_pos) from the natural
@@ -371,10 +373,10 @@ __device__ __forceinline__ void write_nn_row(const RowParams& p, const double* s
     }
 }
 
-__device__ __forceinline__ double tau_pow(double t, double alpha) {
+__device__ __forceinline__ double tau_pow(double t, double alpha, const LibmPowTables* powtab) {
     if (alpha == 1.0) return t;  // pow(x, 1) == x exactly (SURVEY [E1])
     if (alpha == 0.0) return 1.0; // pow(x, 0) == 1 exactly
-    return pow(t, alpha);         // parity unpinned for other alpha
+    return libm_pow(t, alpha, powtab); // the host glibc pow, replayed (libm_pow.cuh)
 }
 
 // One CTA (256 threads) per row.  The elementwise pass works on column PAIRS
@@ -484,8 +486,8 @@ __global__ void __launch_bounds__(256, 3) k_rows(RowParams p) {
                         if constexpr (MODE == MODE_DELTA) drw2[j2] = make_double2(0.0, 0.0);
                     }
                     double2 c;
-                    c.x = (j == i) ? 0.0 : __dmul_rn(tau_pow(t.x, p.alpha), eb[u].x);
-                    c.y = (j + 1 == i) ? 0.0 : __dmul_rn(tau_pow(t.y, p.alpha), eb[u].y);
+                    c.x = (j == i) ? 0.0 : __dmul_rn(tau_pow(t.x, p.alpha, p.powtab), eb[u].x);
+                    c.y = (j + 1 == i) ? 0.0 : __dmul_rn(tau_pow(t.y, p.alpha, p.powtab), eb[u].y);
                     crow2[j2] = c;
                     if (use_row) reinterpret_cast<double2*>(rowbuf)[j2] = c;
                     mx = fmax(mx, fmax(c.x, c.y));
@@ -628,7 +630,7 @@ __global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
                 if (j < n) {
                     const double t = __dadd_rn(__dmul_rn(tv[u], p.keep), rowbuf[j]);
                     trow[j] = t;
-                    const double c = (j == i) ? 0.0 : __dmul_rn(tau_pow(t, p.alpha), eb[u]);
+                    const double c = (j == i) ? 0.0 : __dmul_rn(tau_pow(t, p.alpha, p.powtab), eb[u]);
                     p.choice64[static_cast<size_t>(i) * p.P64 + j] = c;
                     rowbuf[j] = c;
                     mx = fmax(mx, c);
@@ -784,6 +786,13 @@ __global__ void k_philox_test(uint64_t seed, uint32_t it, uint32_t ant, int coun
                               const uint32_t* steps, const uint32_t* draws, double* out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < count) out[i] = philox_uniform(seed, it, ant, steps[i], draws[i]);
+}
+
+// Unit harness for libm_pow (aco_gpu_libm_pow, the creation self-test).
+__global__ void k_libm_pow(const double* __restrict__ xs, const double* __restrict__ ys, int count,
+                           const LibmPowTables* __restrict__ T, double* __restrict__ out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
+        out[i] = libm_pow(xs[i], ys[i], T);
 }
 
 } // namespace acob200

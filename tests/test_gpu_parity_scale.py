@@ -74,24 +74,31 @@ def test_pr2392_full_colony_gather_bit_exact(aco, oracle):
 
 
 def _converged_tau(n, rng):
-    """A late-run pheromone: a strong tour (tau 1) and a weaker second tour
-    (2^-30), every other edge decayed to 2^-U(150, 262) — unused edges after
-    ~150-260 evaporations at rho = 0.5.  Symmetric."""
-    tau = np.exp2(-rng.uniform(150.0, 262.0, size=(n, n)))
-    tau = np.minimum(tau, tau.T)
-    for weight, perm in ((1.0, rng.permutation(n)), (2.0 ** -30, rng.permutation(n))):
-        a, b = perm, np.roll(perm, -1)
-        tau[a, b] = np.maximum(tau[a, b], weight)
-        tau[b, a] = np.maximum(tau[b, a], weight)
-    return tau
+    """A late-run pheromone (symmetric): cities [0, n/2) still mix (tau
+    2^-U(0, 20) among themselves), cities [n/2, n) have converged onto
+    4-cliques (tau 1 inside a clique), and every other edge was unused for
+    250-300 evaporations at rho = 0.5 (tau 2^-U(250, 300)).  Scaled to its
+    row maximum, such an edge lands below the fp32 subnormal range, so a step
+    whose unvisited cities are all of that kind can only be decided by the
+    exact replay, while the mixing half keeps the ordinary fp32/fp64 tiers
+    busy."""
+    h = n // 2
+    tau = np.exp2(-rng.uniform(250.0, 300.0, size=(n, n)))
+    tau[:h, :h] = np.exp2(-rng.uniform(0.0, 20.0, size=(h, h)))
+    perm = h + rng.permutation(n - h)
+    for g in range(0, len(perm) - 3, 4):
+        q = perm[g:g + 4]
+        tau[np.ix_(q, q)] = 1.0
+    return np.minimum(tau, tau.T)
 
 
 def test_late_run_subnormal_regime_tiers_fire_bit_exact(aco, oracle):
-    """pr2392 on the fp32 stream with a converged, wide-range tau (2^-262 ..
+    """pr2392 on the fp32 stream with a converged, wide-range tau (2^-300 ..
     1): the row-scaled fp32 weights of the decayed edges underflow, so the
-    fp32 certification (tier 1) must defer, the fp64 re-sum over the staged
-    row (tier 2) certifies part of it and the exact replay (tier 3) the rest.
-    Both tiers must actually fire, and every tour stays bit-exact."""
+    fp32 certification (tier 1) must defer; the fp64 re-sum over the staged
+    row (tier 2) certifies the rounding-bound cases and the exact replay
+    (tier 3) the underflowed ones.  Both tiers must actually fire, and every
+    tour, length and tau cell stays bit-exact."""
     n, ants = 2392, 384
     prob = aco.build_problem(aco.synthetic_instance(n))
     rng = np.random.default_rng(7)
