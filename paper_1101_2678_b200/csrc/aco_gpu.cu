@@ -136,6 +136,8 @@ struct aco_gpu_ctx {
     long long* h_stats = nullptr;       // pinned: [0..7] d_stats, [8..9] fallback counters
     int32_t* d_tourbuf = nullptr;       // sharded: winning tour exchange buffer (n+1)
     LibmPowTables* d_powtab = nullptr;  // alpha not in {0, 1}: the host libm's pow tables
+    uint8_t* d_qpos = nullptr;          // nn + accumulate: list position of every step's choice
+    double* d_dnn = nullptr;            // nn + accumulate: compact n x nn deposit slots
     ncclComm_t comm = nullptr;
     bool external = false; // world > 1 without an NCCL id: the caller exchanges
     bool sharded = false;  // the sharded protocol (world > 1, or a 1-rank NCCL communicator)
@@ -440,6 +442,7 @@ ConstructParams make_cp(aco_gpu_ctx* c) {
         p.pred_out = c->d_pred + static_cast<size_t>(c->rank) * c->n * c->S;
     }
     p.S = c->S;
+    p.qpos = c->d_qpos;
     return p;
 }
 
@@ -718,9 +721,20 @@ void do_update(aco_gpu_ctx* c) {
         const size_t count2 = static_cast<size_t>(c->n) * c->P64 / 2;
         k_evaporate<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_tau, count2, keep);
         check_launch(c, "k_evaporate");
-        k_deposit_atomic<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_tours, c->d_inv, c->n, c->P64,
-                                                                c->mloc, c->d_tau);
-        check_launch(c, "k_deposit_atomic");
+        if (c->d_dnn) { // nn selection: list edges through the compact slots
+            k_deposit_nn<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_tours, c->d_qpos, c->d_inv, c->n,
+                                                                c->P64, c->mloc, c->cfg.nn, c->d_dnn,
+                                                                c->d_tau);
+            check_launch(c, "k_deposit_nn");
+            const size_t slots = static_cast<size_t>(c->n) * c->cfg.nn;
+            k_apply_nn<<<static_cast<int>(std::min<size_t>((slots + 255) / 256, c->num_sms * 16)), 256, 0,
+                         c->stream>>>(c->d_dnn, c->d_nn, c->n, c->cfg.nn, c->P64, c->d_tau);
+            check_launch(c, "k_apply_nn");
+        } else {
+            k_deposit_atomic<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_tours, c->d_inv, c->n, c->P64,
+                                                                    c->mloc, c->d_tau);
+            check_launch(c, "k_deposit_atomic");
+        }
         CK(cudaEventRecord(c->ev[4], c->stream));
         launch_rows(c, MODE_CHOICE);
     }
@@ -1013,6 +1027,18 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
                 CK(cudaMalloc(&c->d_topk, static_cast<size_t>(n) * kTopK * sizeof(int32_t)));
         }
         const size_t ml = std::max(1, c->mloc);
+        {
+            // nn + accumulate on one context: compact list-edge deposit
+            // (k_deposit_nn); ACO_NN_COMPACT=0 keeps the plain scatter
+            const char* cmp = std::getenv("ACO_NN_COMPACT");
+            if (c->cfg.selection == ACO_SEL_NN && c->cfg.deposit == ACO_DEP_ACCUMULATE && !c->sharded &&
+                !(cmp && cmp[0] == '0')) {
+                CK(cudaMalloc(&c->d_qpos, ml * n));
+                CK(cudaMemset(c->d_qpos, 255, ml * n));
+                CK(cudaMalloc(&c->d_dnn, static_cast<size_t>(n) * c->cfg.nn * sizeof(double)));
+                CK(cudaMemset(c->d_dnn, 0, static_cast<size_t>(n) * c->cfg.nn * sizeof(double)));
+            }
+        }
         CK(cudaMalloc(&c->d_tours, ml * (n + 1) * sizeof(int32_t)));
         CK(cudaMemset(c->d_tours, 0, ml * (n + 1) * sizeof(int32_t)));
         CK(cudaMalloc(&c->d_len, ml * sizeof(int64_t)));
@@ -1114,7 +1140,8 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
     if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
     void* bufs[] = {c->d_choice_nn, c->d_choice_nn32, c->d_nn_scale, c->d_topk, c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
                     c->d_choice_p64, c->d_scale, c->d_nn, c->d_tours, c->d_len, c->d_inv,
-                    c->d_succ, c->d_pred, c->d_delta, c->d_delta32, c->d_stats, c->d_best, c->d_fb, c->d_tourbuf, c->d_verr, c->d_powtab};
+                    c->d_succ, c->d_pred, c->d_delta, c->d_delta32, c->d_stats, c->d_best, c->d_fb, c->d_tourbuf, c->d_verr, c->d_powtab,
+                    c->d_qpos, c->d_dnn};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_stats) cudaFreeHost(c->h_stats);

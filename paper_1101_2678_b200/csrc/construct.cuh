@@ -126,6 +126,11 @@ struct ConstructParams {
     int32_t* succ_out;          // this rank's block of [world][n][S] (gather deposit) or null
     int32_t* pred_out;
     int S;
+    // nn selection + accumulate deposit: per ant-step, the chosen city's
+    // position in the current city's nn list (255: not a list member —
+    // argmax fallback), so k_deposit_nn can fold list edges into the compact
+    // n x nn slot array instead of scattering over n^2 tau
+    uint8_t* qpos;              // mloc x n, or null
 };
 
 // Tour length (tour_length, model.hpp:205-226: an int64 sum, so any order is
@@ -1068,6 +1073,7 @@ __global__ void __launch_bounds__(32, ACO_NN_MINB) k_construct_nn(ConstructParam
             const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
             const float u_up = __double2float_ru(u), u_dn = __double2float_rd(u);
             int next = -1;
+            int qsel = 255;         // list position of next (255: not from the list)
             bool exhausted = false; // every list member visited: argmax fallback
             if (fast32) {
                 // Fast path on the row-scaled fp32 copy of the list weights
@@ -1113,7 +1119,10 @@ __global__ void __launch_bounds__(32, ACO_NN_MINB) k_construct_nn(ConstructParam
                         const float Mt = __fadd_ru(__fmul_ru(nn_ce, __fmul_ru(u_up, Thi)), nn_absq);
                         const float A32 = __fadd_ru(__fadd_ru(__fmul_ru(u_up, T), Mt), 2.0f * nn_absq);
                         const float B32 = __fsub_rd(__fsub_rd(__fmul_rd(u_dn, T), Mt), 2.0f * nn_absq);
-                        if (__fmul_rd(PJ, nn_lo32) > A32 && __fadd_ru(EJ, __fmul_ru(nn_e32, PJ)) < B32) next = Jc;
+                        if (__fmul_rd(PJ, nn_lo32) > A32 && __fadd_ru(EJ, __fmul_ru(nn_e32, PJ)) < B32) {
+                            next = Jc;
+                            qsel = J;
+                        }
                     }
                 }
             } else if (nn <= 32) {
@@ -1147,7 +1156,8 @@ __global__ void __launch_bounds__(32, ACO_NN_MINB) k_construct_nn(ConstructParam
                     }
                     const double T = __shfl_sync(kFull, P, 31);
                     if (!(T > 0.0)) {
-                        next = __shfl_sync(kFull, j, __ffs(unb) - 1); // :89-92, exact
+                        qsel = __ffs(unb) - 1;
+                        next = __shfl_sync(kFull, j, qsel); // :89-92, exact
                     } else {
                         const double Eu = __shfl_up_sync(kFull, P, 1); // every lane shuffles
                         const double E = lane == 0 ? 0.0 : Eu;
@@ -1159,15 +1169,18 @@ __global__ void __launch_bounds__(32, ACO_NN_MINB) k_construct_nn(ConstructParam
                             const double EJ = __shfl_sync(kFull, E, J);
                             const double e = 48.0 * 0x1.0p-53;
                             const double Mt = (e + 0x1.0p-51) * u * T * (1.0 + 0x1.0p-16) + 0x1.0p-1074;
-                            if (PJ * (1.0 - e) > t + Mt && EJ + e * T < t - Mt)
-                                next = __shfl_sync(kFull, j, J);
+                            const int jJ = __shfl_sync(kFull, j, J);
+                            if (PJ * (1.0 - e) > t + Mt && EJ + e * T < t - Mt) {
+                                next = jJ;
+                                qsel = J;
+                            }
                         }
                     }
                 }
             }
             // exact sequential fold: lane q of pass k holds member 32k+q
             double acc = 0.0;
-            int first_un = -1, last_pos = -1;
+            int first_un = -1, last_pos = -1, first_un_q = 255, last_pos_q = 255;
             double mine[2] = {0.0, 0.0};
             int jm[2] = {-1, -1};
 #pragma unroll
@@ -1188,8 +1201,14 @@ __global__ void __launch_bounds__(32, ACO_NN_MINB) k_construct_nn(ConstructParam
                     jm[k] = j;
                     const unsigned unb = __ballot_sync(kFull, un);
                     const unsigned pob = __ballot_sync(kFull, un && w > 0.0);
-                    if (first_un < 0 && unb) first_un = __shfl_sync(kFull, j, __ffs(unb) - 1);
-                    if (pob) last_pos = __shfl_sync(kFull, j, 31 - __clz(pob));
+                    if (first_un < 0 && unb) {
+                        first_un_q = q0 + __ffs(unb) - 1;
+                        first_un = __shfl_sync(kFull, j, __ffs(unb) - 1);
+                    }
+                    if (pob) {
+                        last_pos_q = q0 + 31 - __clz(pob);
+                        last_pos = __shfl_sync(kFull, j, 31 - __clz(pob));
+                    }
                     // lanes >= nn carry w = +0.0, so folding all 32 is exact
                     double wq[32];
 #pragma unroll
@@ -1207,16 +1226,23 @@ __global__ void __launch_bounds__(32, ACO_NN_MINB) k_construct_nn(ConstructParam
                 const double total = acc;
                 if (!(total > 0.0)) {
                     next = first_un;                                     // :89-92
+                    qsel = first_un_q;
                 } else {
                     const double target = u * total;                     // :93
 #pragma unroll
                     for (int k = 0; k < 2 && next < 0; ++k) {
                         if (32 * k < nn) {
                             const unsigned cr = __ballot_sync(kFull, lane + 32 * k < nn && mine[k] > target);
-                            if (cr) next = __shfl_sync(kFull, jm[k], __ffs(cr) - 1);
+                            if (cr) {
+                                next = __shfl_sync(kFull, jm[k], __ffs(cr) - 1);
+                                qsel = 32 * k + __ffs(cr) - 1;
+                            }
                         }
                     }
-                    if (next < 0) next = last_pos >= 0 ? last_pos : first_un; // :103-105
+                    if (next < 0) { // :103-105
+                        next = last_pos >= 0 ? last_pos : first_un;
+                        qsel = last_pos >= 0 ? last_pos_q : first_un_q;
+                    }
                 }
             } else {
                 // argmax over all unvisited, lowest index on ties (:108-120):
@@ -1245,6 +1271,7 @@ __global__ void __launch_bounds__(32, ACO_NN_MINB) k_construct_nn(ConstructParam
                         if (lane == 0) {
                             tabu[next >> 5] |= 1u << (next & 31);
                             tour[step] = next;
+                            if (p.qpos) p.qpos[static_cast<size_t>(kl) * n + step - 1] = 255;
                         }
                         __syncwarp();
                         cur = next;
@@ -1309,12 +1336,14 @@ __global__ void __launch_bounds__(32, ACO_NN_MINB) k_construct_nn(ConstructParam
             if (lane == 0) {
                 tabu[next >> 5] |= 1u << (next & 31);
                 tour[step] = next;
+                if (p.qpos) p.qpos[static_cast<size_t>(kl) * n + step - 1] = static_cast<uint8_t>(qsel);
             }
             __syncwarp();
             cur = next;
         }
         if (lane == 0) {
             tour[n] = start;
+            if (p.qpos) p.qpos[static_cast<size_t>(kl) * n + n - 1] = 255; // the closing edge
             if (fb) atomicAdd(p.argmax_fallbacks, fb);
             if (fb_full) atomicAdd(p.fallbacks, fb_full);
         }

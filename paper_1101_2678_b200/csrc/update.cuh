@@ -279,6 +279,50 @@ __global__ void k_deposit_atomic(const int32_t* __restrict__ tours, const double
     }
 }
 
+// Accumulate deposit for the nn selection (config 5).  An edge a -> b whose
+// head is member q of a's nn list (the construction recorded q) adds w_k to
+// the compact slot dnn[a][q] — n x nn doubles, 2.4 MB at 10k, L2-resident —
+// instead of two reds scattered over the 800 MB tau; every other edge (argmax
+// fallbacks, the closing edge) reds into tau directly.  k_apply_nn then adds
+// each slot to tau[a][b] AND tau[b][a] (the reference deposits w_k on both,
+// pheromone.hpp:198-205) and clears it.  Same sums as deposit_accumulate in
+// a different order: the atomic path's 1e-5 relative contract.
+__global__ void k_deposit_nn(const int32_t* __restrict__ tours, const uint8_t* __restrict__ qpos,
+                             const double* __restrict__ inv, int n, int P64, int mloc, int nn,
+                             double* __restrict__ dnn, double* __restrict__ tau) {
+    const size_t total = static_cast<size_t>(mloc) * n;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int kl = static_cast<int>(i / n), s = static_cast<int>(i - static_cast<size_t>(kl) * n);
+        const int32_t* t = tours + static_cast<size_t>(kl) * (n + 1);
+        const int a = t[s];
+        const int q = qpos[i];
+        const double w = inv[kl];
+        if (q < nn) {
+            atomicAdd(dnn + static_cast<size_t>(a) * nn + q, w);
+        } else {
+            const int b = t[s + 1];
+            atomicAdd(tau + static_cast<size_t>(a) * P64 + b, w);
+            atomicAdd(tau + static_cast<size_t>(b) * P64 + a, w);
+        }
+    }
+}
+
+__global__ void k_apply_nn(double* __restrict__ dnn, const int32_t* __restrict__ nn_lists, int n,
+                           int nn, int P64, double* __restrict__ tau) {
+    const size_t slots = static_cast<size_t>(n) * nn;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < slots;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const double d = dnn[i];
+        if (d != 0.0) {
+            const int a = static_cast<int>(i / nn), b = nn_lists[i];
+            atomicAdd(tau + static_cast<size_t>(a) * P64 + b, d);
+            atomicAdd(tau + static_cast<size_t>(b) * P64 + a, d);
+            dnn[i] = 0.0;
+        }
+    }
+}
+
 // MODE_DELTA32: MODE_DELTA reading the fp32 all-reduced delta (NCCL fp32
 // wire; k_delta_pack already zeroed the fp64 delta)
 enum { MODE_CHOICE = 0, MODE_GATHER = 1, MODE_DELTA = 2, MODE_DELTA32 = 3 };

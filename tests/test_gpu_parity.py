@@ -568,3 +568,32 @@ def test_nn_long_lists_bit_exact(aco, oracle, nn):
             assert np.array_equal(eng.ants()[0], t_ref), f"iteration {it}"
             tau = oracle.update(tau, t_ref, l_ref, 0.5, 1)
             assert np.array_equal(eng.pheromone(), tau)
+
+
+@pytest.mark.parametrize("n,nn,ants", [(1002, 30, None), (3000, 8, (0, 400))])
+@pytest.mark.parametrize("compact", ["1", "0"])
+def test_nn_accumulate_compact_deposit_within_tolerance(aco, oracle, monkeypatch, n, nn, ants,
+                                                        compact):
+    """nn selection + accumulate: list edges fold into the compact n x nn
+    slots (k_deposit_nn + k_apply_nn), the rest scatter into tau — tau within
+    1e-5 relative of deposit_accumulate (pheromone.hpp:195-208) from a shared
+    state each iteration, tours bit-exact; ACO_NN_COMPACT=0 is the plain
+    scatter.  n=3000/nn=8 makes argmax fallbacks (non-list edges) frequent."""
+    monkeypatch.setenv("ACO_NN_COMPACT", compact)
+    prob, eng = make(aco, n, selection=1, deposit=0, nn=nn, ant_range=ants)
+    k0, k1 = ants or (0, n)
+    with eng:
+        nnl = oracle.nn_lists(prob.dist, nn)
+        tau = np.full((n, n), eng.tau0)
+        for it in range(3):
+            eng.set_pheromone(tau)
+            ch = oracle.choice(prob.dist, tau)
+            eng.run_iteration()
+            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, k0, k1, selection=1,
+                                               nn_lists=nnl)
+            t, l = eng.ants()
+            assert np.array_equal(t, t_ref), f"iteration {it}"
+            tau_ref = oracle.update(tau, t_ref, l_ref, 0.5, 0)
+            got = eng.pheromone()
+            assert (np.abs(got - tau_ref) / np.abs(tau_ref)).max() <= ATOMIC_RTOL
+            tau = tau_ref
