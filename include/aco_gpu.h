@@ -105,12 +105,21 @@ typedef struct {
     int32_t rank, world;
     int32_t ant_begin, ant_end;
     uint8_t nccl_id[128];
-    /* Datatype of the sharded accumulate path's delta-tau all-reduce:
-     * ACO_WIRE_FP64 (default) keeps the reference's fp64 reals end to end
-     * (ranks differ from a single-GPU colony only by the atomic order,
-     * ~1e-16); ACO_WIRE_FP32 halves the wire bytes at one 2^-24 rounding of
-     * every delta per iteration, so tours after iteration 0 may then depend
-     * on the GPU count.  Every rank of a colony must pass the same value. */
+    /* Accumulate-deposit arithmetic and (sharded) delta-tau exchange:
+     *  ACO_WIRE_FP64 (default): fp64 reds; sharded: fp64 all-reduce of the
+     *    local delta (ranks differ from a single-GPU colony only by the
+     *    atomic order, ~1e-16);
+     *  ACO_WIRE_FP32: sharded only, fp32 all-reduce (half the bytes, one
+     *    2^-24 rounding per delta: tours after iteration 0 may depend on G);
+     *  ACO_WIRE_FIXED64: every deposit as an exact int64 fixed-point sum
+     *    (scale from the iteration's best length) — order-free, so tau is
+     *    bit-identical run to run, on every rank and for every G; sharded:
+     *    ncclUint64 all-reduce;
+     *  ACO_WIRE_MULTIMEM: FIXED64 whose deposit reds go straight into an NVLS
+     *    multicast object (every GPU's delta at once, multimem.red.add.u64)
+     *    with a flag barrier through the same object: no collective (needs
+     *    world > 1 on one NVSwitch node; world == 1 runs FIXED64).
+     * Every rank of a colony must pass the same value. */
     int32_t wire;
     /* Debug mode (TourBuffer::make pheromone.hpp:67-90 and
      * tour_length model.hpp:205-220): every construction is followed by a
@@ -120,7 +129,7 @@ typedef struct {
     int32_t validate_tours;
 } aco_gpu_params;
 
-enum { ACO_WIRE_FP64 = 0, ACO_WIRE_FP32 = 1 };
+enum { ACO_WIRE_FP64 = 0, ACO_WIRE_FP32 = 1, ACO_WIRE_FIXED64 = 2, ACO_WIRE_MULTIMEM = 3 };
 
 /* aco::IterationRecord (engine.hpp:31-38) + device timings. */
 typedef struct {

@@ -20,6 +20,8 @@ ACO_E_NCCL = 101
 ACO_E_UNSUPPORTED = 102
 ACO_WIRE_FP64 = 0
 ACO_WIRE_FP32 = 1
+ACO_WIRE_FIXED64 = 2
+ACO_WIRE_MULTIMEM = 3
 
 
 class aco_gpu_params(C.Structure):

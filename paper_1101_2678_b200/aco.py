@@ -91,9 +91,11 @@ class WeightStream(enum.IntEnum):  # include/aco_gpu.h ACO_STREAM_*
     fp32 = 2
 
 
-class Wire(enum.IntEnum):  # include/aco_gpu.h ACO_WIRE_*: sharded accumulate delta all-reduce
-    fp64 = 0
-    fp32 = 1
+class Wire(enum.IntEnum):  # include/aco_gpu.h ACO_WIRE_*: accumulate arithmetic / delta exchange
+    fp64 = 0      # fp64 reds; sharded: fp64 all-reduce
+    fp32 = 1      # sharded: fp32 all-reduce (tours may then depend on world)
+    fixed64 = 2   # exact int64 fixed-point sums: tau bit-identical for every world
+    multimem = 3  # fixed64 through an NVLS multicast object, no collective (world > 1)
 
 
 def selection_name(s: Selection) -> str:  # construction.hpp:15

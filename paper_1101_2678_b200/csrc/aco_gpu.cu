@@ -4,6 +4,7 @@
 // choice, tours, lengths, best tour) stays resident in HBM/L2; the host only
 // sees what the caller asks for.  Multi-GPU sharding uses NCCL,
 // loaded at run time with dlopen so a single-GPU process never needs it.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -16,6 +17,7 @@
 #include <cstring>
 #include <limits>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/aco_gpu.h"
@@ -69,6 +71,60 @@ NcclApi& nccl() {
         }
     }
     return api;
+}
+
+// CUDA driver entry points for the NVLS multicast exchange (f2), resolved
+// through the runtime so libaco_gpu.so never links libcuda directly.
+struct DriverApi {
+    bool loaded = false;
+    CUresult (*MulticastGetGranularity)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags) = nullptr;
+    CUresult (*MulticastCreate)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*) = nullptr;
+    CUresult (*MulticastAddDevice)(CUmemGenericAllocationHandle, CUdevice) = nullptr;
+    CUresult (*MulticastBindMem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                                 unsigned long long) = nullptr;
+    CUresult (*MulticastUnbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t) = nullptr;
+    CUresult (*MemCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+    CUresult (*MemRelease)(CUmemGenericAllocationHandle) = nullptr;
+    CUresult (*MemExportToShareableHandle)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType,
+                                           unsigned long long) = nullptr;
+    CUresult (*MemImportFromShareableHandle)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType) = nullptr;
+    CUresult (*MemAddressReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+    CUresult (*MemAddressFree)(CUdeviceptr, size_t) = nullptr;
+    CUresult (*MemMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+    CUresult (*MemUnmap)(CUdeviceptr, size_t) = nullptr;
+    CUresult (*MemSetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+    CUresult (*GetErrorName)(CUresult, const char**) = nullptr;
+};
+
+DriverApi& driver() {
+    static DriverApi d;
+    if (!d.loaded) {
+        d.loaded = true;
+        auto get = [](const char* name, auto& fn) {
+            void* p = nullptr;
+            cudaDriverEntryPointQueryResult q{};
+            if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(p);
+            cudaGetLastError();
+        };
+        get("cuMulticastGetGranularity", d.MulticastGetGranularity);
+        get("cuMulticastCreate", d.MulticastCreate);
+        get("cuMulticastAddDevice", d.MulticastAddDevice);
+        get("cuMulticastBindMem", d.MulticastBindMem);
+        get("cuMulticastUnbind", d.MulticastUnbind);
+        get("cuMemCreate", d.MemCreate);
+        get("cuMemRelease", d.MemRelease);
+        get("cuMemExportToShareableHandle", d.MemExportToShareableHandle);
+        get("cuMemImportFromShareableHandle", d.MemImportFromShareableHandle);
+        get("cuMemAddressReserve", d.MemAddressReserve);
+        get("cuMemAddressFree", d.MemAddressFree);
+        get("cuMemMap", d.MemMap);
+        get("cuMemUnmap", d.MemUnmap);
+        get("cuMemSetAccess", d.MemSetAccess);
+        get("cuGetErrorName", d.GetErrorName);
+    }
+    return d;
 }
 
 thread_local std::string g_host_err;
@@ -136,6 +192,15 @@ struct aco_gpu_ctx {
     long long* h_stats = nullptr;       // pinned: [0..7] d_stats, [8..9] fallback counters
     int32_t* d_tourbuf = nullptr;       // sharded: winning tour exchange buffer (n+1)
     LibmPowTables* d_powtab = nullptr;  // alpha not in {0, 1}: the host libm's pow tables
+    // fixed-point accumulate (wire FIXED64 / MULTIMEM): exact int64 delta sums
+    bool fixed = false;
+    bool multimem = false;              // NVLS multicast exchange (world > 1)
+    unsigned long long* d_delta_fix = nullptr; // n x P64 (or the multicast object's local memory)
+    // NVLS multicast object (f2): delta + barrier flag, local (uc) and multicast (mc) views
+    CUmemGenericAllocationHandle mc_handle = 0, mc_phys = 0;
+    CUdeviceptr mc_uc = 0, mc_va = 0;
+    size_t mc_size = 0;
+    unsigned long long mc_epoch = 0;
     uint8_t* d_qpos = nullptr;          // nn + accumulate: list position of every step's choice
     double* d_dnn = nullptr;            // nn + accumulate: compact n x nn deposit slots
     ncclComm_t comm = nullptr;
@@ -361,6 +426,8 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
     rp.alpha = c->cfg.alpha;
     rp.keep = 1.0 - c->cfg.rho; // pheromone.hpp:179
     rp.powtab = c->d_powtab;
+    rp.delta_fix = c->d_delta_fix;
+    rp.stats = c->d_stats;
     const size_t smem = static_cast<size_t>(c->P64) * sizeof(double);
     const size_t wsmem = smem + 64 * sizeof(double);
     if (mode == MODE_GATHER && wsmem <= 32 * 1024) { // one warp per row
@@ -396,10 +463,12 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
         CK(cudaFuncSetAttribute(k_rows<MODE_GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute(k_rows<MODE_DELTA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute(k_rows<MODE_DELTA32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k_rows<MODE_DELTA_FIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
     if (mode == MODE_CHOICE) k_rows<MODE_CHOICE><<<grid, 256, rsmem, c->stream>>>(rp);
     else if (mode == MODE_GATHER) k_rows<MODE_GATHER><<<grid, 256, rsmem, c->stream>>>(rp);
     else if (mode == MODE_DELTA32) k_rows<MODE_DELTA32><<<grid, 256, rsmem, c->stream>>>(rp);
+    else if (mode == MODE_DELTA_FIX) k_rows<MODE_DELTA_FIX><<<grid, 256, rsmem, c->stream>>>(rp);
     else k_rows<MODE_DELTA><<<grid, 256, rsmem, c->stream>>>(rp);
     check_launch(c, "k_rows");
     launch_topk(c);
@@ -542,6 +611,106 @@ void launch_construct(aco_gpu_ctx* c) {
 }
 
 
+// ---- NVLS multicast object for the fused exchange (wire MULTIMEM, f2) -----
+// Rank 0 creates a multicast object over `world` devices and exports it as a
+// fabric handle; the handle travels to the other ranks over the engine's own
+// NCCL communicator (ncclBroadcast); every rank imports it, adds its device,
+// and — after a barrier, so all devices are members before any memory is
+// bound — binds a local physical allocation (the delta + barrier flag) and
+// maps both views: unicast (its own memory, read by k_rows) and multicast
+// (the address k_deposit_fixed<true> and k_mc_barrier red into).
+void mc_check(CUresult r, const char* what) {
+    if (r != CUDA_SUCCESS) {
+        const char* name = nullptr;
+        if (driver().GetErrorName) driver().GetErrorName(r, &name);
+        throw Fail{ACO_E_UNSUPPORTED, std::string("NVLS multicast exchange: ") + what + " -> " +
+                                          (name ? name : "CUDA driver error")};
+    }
+}
+
+void nccl_barrier(aco_gpu_ctx* c) {
+    int32_t* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(int32_t)));
+    CK(cudaMemsetAsync(d, 0, sizeof(int32_t), c->stream));
+    NK(nccl().AllReduce(d, d, 1, ncclInt32, ncclSum, c->comm, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(d);
+}
+
+void setup_multicast(aco_gpu_ctx* c) {
+    DriverApi& d = driver();
+    if (!d.MulticastCreate || !d.MulticastBindMem || !d.MemImportFromShareableHandle)
+        throw Fail{ACO_E_UNSUPPORTED, "NVLS multicast exchange: driver entry points unavailable"};
+    const CUmemAllocationHandleType ht = CU_MEM_HANDLE_TYPE_FABRIC;
+    const size_t cells = static_cast<size_t>(c->n) * c->P64;
+    const size_t want = cells * sizeof(unsigned long long) + 256; // delta + barrier flag
+    CUmulticastObjectProp mp{};
+    mp.numDevices = static_cast<unsigned int>(c->world);
+    mp.handleTypes = ht;
+    mp.size = want;
+    size_t gran = 0;
+    mc_check(d.MulticastGetGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED),
+             "cuMulticastGetGranularity");
+    c->mc_size = (want + gran - 1) / gran * gran;
+    mp.size = c->mc_size;
+    CUmemFabricHandle fh{};
+    if (c->rank == 0) {
+        mc_check(d.MulticastCreate(&c->mc_handle, &mp), "cuMulticastCreate");
+        mc_check(d.MemExportToShareableHandle(&fh, c->mc_handle, ht, 0), "cuMemExportToShareableHandle");
+    }
+    uint8_t* dh = nullptr;
+    CK(cudaMalloc(&dh, sizeof(fh)));
+    CK(cudaMemcpyAsync(dh, &fh, sizeof(fh), cudaMemcpyHostToDevice, c->stream));
+    NK(nccl().Broadcast(dh, dh, sizeof(fh), ncclUint8, 0, c->comm, c->stream));
+    CK(cudaMemcpyAsync(&fh, dh, sizeof(fh), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(dh);
+    if (c->rank != 0)
+        mc_check(d.MemImportFromShareableHandle(&c->mc_handle, &fh, ht), "cuMemImportFromShareableHandle");
+    mc_check(d.MulticastAddDevice(c->mc_handle, static_cast<CUdevice>(c->device)), "cuMulticastAddDevice");
+    nccl_barrier(c); // every device joined before any memory is bound
+    CUmemAllocationProp ap{};
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = c->device;
+    ap.requestedHandleTypes = ht;
+    mc_check(d.MemCreate(&c->mc_phys, c->mc_size, &ap, 0), "cuMemCreate");
+    mc_check(d.MulticastBindMem(c->mc_handle, 0, c->mc_phys, 0, c->mc_size, 0), "cuMulticastBindMem");
+    CUmemAccessDesc acc{};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = c->device;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    mc_check(d.MemAddressReserve(&c->mc_uc, c->mc_size, gran, 0, 0), "cuMemAddressReserve");
+    mc_check(d.MemMap(c->mc_uc, c->mc_size, 0, c->mc_phys, 0), "cuMemMap(unicast)");
+    mc_check(d.MemSetAccess(c->mc_uc, c->mc_size, &acc, 1), "cuMemSetAccess(unicast)");
+    mc_check(d.MemAddressReserve(&c->mc_va, c->mc_size, gran, 0, 0), "cuMemAddressReserve");
+    mc_check(d.MemMap(c->mc_va, c->mc_size, 0, c->mc_handle, 0), "cuMemMap(multicast)");
+    mc_check(d.MemSetAccess(c->mc_va, c->mc_size, &acc, 1), "cuMemSetAccess(multicast)");
+    CK(cudaMemsetAsync(reinterpret_cast<void*>(c->mc_uc), 0, c->mc_size, c->stream));
+    nccl_barrier(c); // zeroed everywhere before the first red arrives
+    c->d_delta_fix = reinterpret_cast<unsigned long long*>(c->mc_uc);
+    c->multimem = true;
+}
+
+void teardown_multicast(aco_gpu_ctx* c) {
+    DriverApi& d = driver();
+    if (c->mc_va && d.MemUnmap) {
+        d.MemUnmap(c->mc_va, c->mc_size);
+        d.MemAddressFree(c->mc_va, c->mc_size);
+    }
+    if (c->mc_uc && d.MemUnmap) {
+        d.MemUnmap(c->mc_uc, c->mc_size);
+        d.MemAddressFree(c->mc_uc, c->mc_size);
+    }
+    if (c->mc_handle && c->mc_phys && d.MulticastUnbind)
+        d.MulticastUnbind(c->mc_handle, static_cast<CUdevice>(c->device), 0, c->mc_size);
+    if (c->mc_phys && d.MemRelease) d.MemRelease(c->mc_phys);
+    if (c->mc_handle && d.MemRelease) d.MemRelease(c->mc_handle);
+    c->mc_va = c->mc_uc = 0;
+    c->mc_phys = c->mc_handle = 0;
+    c->d_delta_fix = nullptr;
+}
+
 // pow(tau, alpha) for alpha not in {0, 1}: upload the host libm's pow tables
 // and prove on this device that libm_pow replays the host's std::pow on a
 // spread of pheromone-like arguments (tau0-scaled, down through the
@@ -675,7 +844,7 @@ void do_construct(aco_gpu_ctx* c) {
         c->d_len, c->mloc, c->d_tours, c->n, c->d_stats, c->d_stats + 3, c->d_best,
         c->sharded ? 0 : 1);
     check_launch(c, "k_iter_stats");
-    if (c->sharded && !gather_mode(c)) { // local delta for the all-reduce
+    if (c->sharded && !gather_mode(c) && !c->fixed) { // local delta for the all-reduce
         k_deposit_atomic<<<c->num_sms * 8, 256, 0, c->stream>>>(
             c->d_tours, c->d_inv + static_cast<size_t>(c->rank) * c->S, c->n, c->P64, c->mloc,
             c->d_delta);
@@ -685,8 +854,52 @@ void do_construct(aco_gpu_ctx* c) {
 }
 
 // exchange + evaporate + deposit + choice (no host sync)
+// Fixed-point accumulate: exact int64 delta sums (k_deposit_fixed), then one
+// fused evaporate + delta + choice pass (k_rows<DELTA_FIX>).  Sharded: an
+// ncclUint64 all-reduce of the delta (wire FIXED64, exact), or — wire
+// MULTIMEM, f2 — the deposit's reds go straight to the NVLS multicast object
+// (every GPU's delta at once) and a flag barrier through the same object
+// replaces the collective.
+void do_update_fixed(aco_gpu_ctx* c) {
+    const bool shard = c->sharded && !c->external;
+    const int shift = c->key_two_stage ? 0 : c->key_shift;
+    k_fixed_scale<<<1, 32, 0, c->stream>>>(c->d_stats, c->m, shift, shard ? 1 : 0);
+    check_launch(c, "k_fixed_scale");
+    const double* inv = c->d_inv + static_cast<size_t>(c->rank) * c->S;
+    if (c->multimem) {
+        k_deposit_fixed<true><<<c->num_sms * 8, 256, 0, c->stream>>>(
+            c->d_tours, inv, c->n, c->P64, c->mloc, c->d_stats,
+            reinterpret_cast<unsigned long long*>(c->mc_va));
+        check_launch(c, "k_deposit_fixed<multimem>");
+        const size_t flag_off = static_cast<size_t>(c->n) * c->P64 * sizeof(unsigned long long);
+        ++c->mc_epoch;
+        k_mc_barrier<<<1, 32, 0, c->stream>>>(
+            reinterpret_cast<unsigned long long*>(c->mc_va + flag_off),
+            reinterpret_cast<const unsigned long long*>(c->mc_uc + flag_off),
+            c->mc_epoch * static_cast<unsigned long long>(c->world));
+        check_launch(c, "k_mc_barrier");
+    } else {
+        k_deposit_fixed<false><<<c->num_sms * 8, 256, 0, c->stream>>>(
+            c->d_tours, inv, c->n, c->P64, c->mloc, c->d_stats, c->d_delta_fix);
+        check_launch(c, "k_deposit_fixed");
+        if (shard) {
+            const size_t cells = static_cast<size_t>(c->n) * c->P64;
+            NK(nccl().AllReduce(c->d_delta_fix, c->d_delta_fix, cells, ncclUint64, ncclSum, c->comm,
+                                c->stream));
+        }
+    }
+    CK(cudaEventRecord(c->ev[3], c->stream));
+    launch_rows(c, MODE_DELTA_FIX);
+    CK(cudaEventRecord(c->ev[4], c->stream));
+    CK(cudaEventRecord(c->ev[5], c->stream));
+}
+
 void do_update(aco_gpu_ctx* c) {
     const double keep = 1.0 - c->cfg.rho;
+    if (c->fixed) {
+        do_update_fixed(c);
+        return;
+    }
     if (c->sharded && !c->external) {
         auto& api = nccl();
         if (gather_mode(c)) {
@@ -1027,12 +1240,19 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
                 CK(cudaMalloc(&c->d_topk, static_cast<size_t>(n) * kTopK * sizeof(int32_t)));
         }
         const size_t ml = std::max(1, c->mloc);
+        if (prm->wire < ACO_WIRE_FP64 || prm->wire > ACO_WIRE_MULTIMEM)
+            throw ModelError(Errc::config_error, "unknown wire");
+        c->fixed = c->cfg.deposit == ACO_DEP_ACCUMULATE &&
+                   (prm->wire == ACO_WIRE_FIXED64 || prm->wire == ACO_WIRE_MULTIMEM);
+        if (c->fixed && c->external)
+            throw ModelError(Errc::config_error,
+                             "fixed-point / multimem exchange needs the engine's own NCCL communicator");
         {
             // nn + accumulate on one context: compact list-edge deposit
             // (k_deposit_nn); ACO_NN_COMPACT=0 keeps the plain scatter
             const char* cmp = std::getenv("ACO_NN_COMPACT");
             if (c->cfg.selection == ACO_SEL_NN && c->cfg.deposit == ACO_DEP_ACCUMULATE && !c->sharded &&
-                !(cmp && cmp[0] == '0')) {
+                !c->fixed && !(cmp && cmp[0] == '0')) {
                 CK(cudaMalloc(&c->d_qpos, ml * n));
                 CK(cudaMemset(c->d_qpos, 255, ml * n));
                 CK(cudaMalloc(&c->d_dnn, static_cast<size_t>(n) * c->cfg.nn * sizeof(double)));
@@ -1055,7 +1275,12 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         const char* gsplit = std::getenv("ACO_GATHER_SPLIT");
         const bool warp_gather = c->cfg.deposit != ACO_DEP_ACCUMULATE &&
                                  static_cast<size_t>(c->P64) * sizeof(double) + 64 * sizeof(double) <= 32 * 1024;
-        if ((c->sharded && c->cfg.deposit == ACO_DEP_ACCUMULATE) ||
+        const bool mc_wanted = c->fixed && prm->wire == ACO_WIRE_MULTIMEM && c->world > 1;
+        if (c->fixed && !mc_wanted) { // exact int64 delta (one GPU, or the ncclUint64 all-reduce)
+            CK(cudaMalloc(&c->d_delta_fix, cells * sizeof(unsigned long long)));
+            CK(cudaMemset(c->d_delta_fix, 0, cells * sizeof(unsigned long long)));
+        }
+        if ((c->sharded && c->cfg.deposit == ACO_DEP_ACCUMULATE && !c->fixed) ||
             (warp_gather && !(gsplit && gsplit[0] == '0'))) {
             CK(cudaMalloc(&c->d_delta, cells * sizeof(double)));
             CK(cudaMemset(c->d_delta, 0, cells * sizeof(double)));
@@ -1096,6 +1321,7 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
             ncclUniqueId id;
             std::memcpy(&id, prm->nccl_id, sizeof(id));
             NK(api.CommInitRank(&c->comm, c->world, id, c->rank));
+            if (mc_wanted) setup_multicast(c);
         }
 
         if (c->cfg.alpha != 0.0 && c->cfg.alpha != 1.0) {
@@ -1137,11 +1363,12 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
 #endif
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    if (c->multimem) teardown_multicast(c);
     if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
     void* bufs[] = {c->d_choice_nn, c->d_choice_nn32, c->d_nn_scale, c->d_topk, c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
                     c->d_choice_p64, c->d_scale, c->d_nn, c->d_tours, c->d_len, c->d_inv,
                     c->d_succ, c->d_pred, c->d_delta, c->d_delta32, c->d_stats, c->d_best, c->d_fb, c->d_tourbuf, c->d_verr, c->d_powtab,
-                    c->d_qpos, c->d_dnn};
+                    c->d_qpos, c->d_dnn, c->d_delta_fix};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_stats) cudaFreeHost(c->h_stats);

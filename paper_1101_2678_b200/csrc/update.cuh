@@ -323,9 +323,80 @@ __global__ void k_apply_nn(double* __restrict__ dnn, const int32_t* __restrict__
     }
 }
 
+// ---- fixed-point accumulate (ACO_WIRE_FIXED64 / ACO_WIRE_MULTIMEM) -------
+// Every deposit w_k = 1/C_k is added as the integer round(w_k * 2^s) with
+// 64-bit integer reds, so each cell's delta is an EXACT integer sum: the
+// result does not depend on the order of the reds, on the number of GPUs or
+// on how an all-reduce (ncclInt64) or the NVSwitch (multimem) combines them
+// — tau is bit-identical on every rank and for every G.  s is chosen per
+// iteration from the colony's best length L (k_fixed_scale): no cell can
+// receive more than sum_k w_k <= m / L (an edge is used at most twice per
+// tour), so with S = 2m/L < 2^(e+1), s = 60 - e keeps every sum below 2^61.
+// Per contribution the rounding is <= 2^-(s+1), i.e. relative <= m * (C_max /
+// C_min) * 2^-61 ~ 1e-14 at 10^4 ants — far inside the atomic path's 1e-5
+// relative contract (pheromone.hpp:195-208, deposit_accumulate).
+// stats[7] receives s (or -1: a zero-length tour, 1/C_k = inf, which no
+// fixed-point scale represents — the engine then fails the iteration).
+__global__ void k_fixed_scale(long long* stats, int m, int shard_shift, int sharded) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const long long L = sharded ? shard_best_len(stats, shard_shift) : stats[0];
+    if (L <= 0) {
+        stats[7] = -1;
+        return;
+    }
+    const double S = 2.0 * static_cast<double>(m) / static_cast<double>(L);
+    stats[7] = 60 - ilogb(S);
+}
+
+template <bool MULTIMEM>
+__device__ __forceinline__ void red_u64(unsigned long long* addr, unsigned long long v) {
+    if constexpr (MULTIMEM) {
+        // NVLS: one red to the multicast address, applied by the NVSwitch to
+        // the delta of every GPU bound to the object
+        asm volatile("multimem.red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(addr), "l"(v) : "memory");
+    } else {
+        atomicAdd(addr, v);
+    }
+}
+
+template <bool MULTIMEM>
+__global__ void k_deposit_fixed(const int32_t* __restrict__ tours, const double* __restrict__ inv,
+                                int n, int P64, int mloc, const long long* __restrict__ stats,
+                                unsigned long long* __restrict__ target) {
+    const int sh = static_cast<int>(stats[7]);
+    if (sh < 0) return;
+    const size_t total = static_cast<size_t>(mloc) * n;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int kl = static_cast<int>(i / n), s = static_cast<int>(i - static_cast<size_t>(kl) * n);
+        const int32_t* t = tours + static_cast<size_t>(kl) * (n + 1);
+        const int a = t[s], b = t[s + 1];
+        const unsigned long long v = __double2ull_rn(scalbn(inv[kl], sh));
+        red_u64<MULTIMEM>(target + static_cast<size_t>(a) * P64 + b, v);
+        red_u64<MULTIMEM>(target + static_cast<size_t>(b) * P64 + a, v);
+    }
+}
+
+// Cross-GPU barrier over the multicast object (ACO_WIRE_MULTIMEM), one
+// thread: make this GPU's reds visible system-wide, add 1 to every GPU's copy
+// of the flag with one release red through the switch, then wait until the
+// local copy shows all `world` arrivals of this epoch.
+__global__ void k_mc_barrier(unsigned long long* mc_flag, const unsigned long long* uc_flag,
+                             unsigned long long target) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    asm volatile("multimem.red.release.sys.global.add.u64 [%0], %1;" ::"l"(mc_flag), "l"(1ull) : "memory");
+    unsigned long long v = 0;
+    do {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(uc_flag) : "memory");
+    } while (v < target);
+}
+
 // MODE_DELTA32: MODE_DELTA reading the fp32 all-reduced delta (NCCL fp32
 // wire; k_delta_pack already zeroed the fp64 delta)
-enum { MODE_CHOICE = 0, MODE_GATHER = 1, MODE_DELTA = 2, MODE_DELTA32 = 3 };
+// MODE_DELTA_FIX: tau = fl(fl(tau*keep) + delta_i64 * 2^-s) from the exact
+// fixed-point sums (k_deposit_fixed), then clears the delta.
+enum { MODE_CHOICE = 0, MODE_GATHER = 1, MODE_DELTA = 2, MODE_DELTA32 = 3, MODE_DELTA_FIX = 4 };
 
 struct RowParams {
     double* tau;             // n x P64
@@ -350,6 +421,8 @@ struct RowParams {
     int shards, S, m;        // ants: shard g holds global ants [g*S, min(m,(g+1)*S))
     double alpha, keep;
     const LibmPowTables* powtab; // host libm's pow tables (alpha not in {0, 1})
+    unsigned long long* delta_fix; // MODE_DELTA_FIX: n x P64 fixed-point sums
+    const long long* stats;        // MODE_DELTA_FIX: stats[7] = the scale exponent s
 };
 
 // Write one row of the permuted streamed layout (stream_pos) from the natural
@@ -488,6 +561,10 @@ __global__ void __launch_bounds__(256, 3) k_rows(RowParams p) {
         double2* drw2 = MODE == MODE_DELTA
                             ? reinterpret_cast<double2*>(p.delta + static_cast<size_t>(i) * p.P64)
                             : nullptr;
+        ulonglong2* dfx2 = MODE == MODE_DELTA_FIX
+                               ? reinterpret_cast<ulonglong2*>(p.delta_fix + static_cast<size_t>(i) * p.P64)
+                               : nullptr;
+        const int fsh = MODE == MODE_DELTA_FIX ? static_cast<int>(p.stats[7]) : 0;
         for (int b0 = tid; b0 < n2; b0 += 256 * EB) {
             double2 tv[EB], dl[EB], eb[EB];
             int2 dv[EB];
@@ -498,6 +575,11 @@ __global__ void __launch_bounds__(256, 3) k_rows(RowParams p) {
                 tv[u] = in ? trow2[j2] : make_double2(0.0, 0.0);
                 dv[u] = (in && !erow2) ? __ldg(drow2 + j2) : make_int2(0, 0);
                 if constexpr (MODE == MODE_DELTA) dl[u] = in ? drw2[j2] : make_double2(0.0, 0.0);
+                if constexpr (MODE == MODE_DELTA_FIX) {
+                    const ulonglong2 f = in ? dfx2[j2] : make_ulonglong2(0ull, 0ull);
+                    // exact integer sum -> double (one rounding) -> exact 2^-s scaling
+                    dl[u] = make_double2(scalbn(__ull2double_rn(f.x), -fsh), scalbn(__ull2double_rn(f.y), -fsh));
+                }
                 if constexpr (MODE == MODE_DELTA32) {
                     const float2 f = in ? reinterpret_cast<const float2*>(
                                               p.delta32 + static_cast<size_t>(i) * p.P64)[j2]
@@ -522,12 +604,14 @@ __global__ void __launch_bounds__(256, 3) k_rows(RowParams p) {
                 if (j2 < n2) {
                     const int j = 2 * j2;
                     double2 t = tv[u];
-                    if constexpr (MODE == MODE_GATHER || MODE == MODE_DELTA || MODE == MODE_DELTA32) {
+                    if constexpr (MODE == MODE_GATHER || MODE == MODE_DELTA || MODE == MODE_DELTA32 ||
+                                  MODE == MODE_DELTA_FIX) {
                         // pheromone.hpp:183 (evaporate) then :220 / the summed delta
                         t.x = __dadd_rn(__dmul_rn(t.x, p.keep), dl[u].x);
                         t.y = __dadd_rn(__dmul_rn(t.y, p.keep), dl[u].y);
                         trow2[j2] = t;
                         if constexpr (MODE == MODE_DELTA) drw2[j2] = make_double2(0.0, 0.0);
+                        if constexpr (MODE == MODE_DELTA_FIX) dfx2[j2] = make_ulonglong2(0ull, 0ull);
                     }
                     double2 c;
                     c.x = (j == i) ? 0.0 : __dmul_rn(tau_pow(t.x, p.alpha, p.powtab), eb[u].x);

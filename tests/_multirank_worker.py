@@ -39,7 +39,7 @@ def main():
     obj = [aco.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     eng = aco.Engine(prob, cfg(rank=rank, world=world, nccl_id=obj[0]))
-    single = aco.Engine(prob, cfg()) if rank == 0 else None
+    single = aco.Engine(prob, cfg()) if rank == 0 else None  # same wire (fp32 is sharded-only)
     report = {"world": world, "deposit": deposit, "wire": wire, "iterations": []}
     for it in range(iters):
         rec = eng.run_iteration()

@@ -134,3 +134,67 @@ def test_nccl_exchange_path_one_rank(deposit, wire):
             nccl.set_pheromone(pa)  # fp32 wire: keep the construction inputs identical
     plain.close()
     nccl.close()
+
+
+@pytest.mark.parametrize("wire", [2, 3])
+def test_fixed_point_exchange_bit_identical_for_any_world(wire):
+    """ACO_WIRE_FIXED64 / MULTIMEM: every deposit is an exact int64
+    fixed-point sum, so tau does not depend on the order of the reds or on
+    the exchange.  The sharded protocol on a one-rank NCCL communicator
+    (ncclUint64 all-reduce; MULTIMEM at world 1 runs the same FIXED64 path —
+    its multicast object needs >= 2 GPUs) reproduces the single-context
+    fixed-point colony BIT FOR BIT over a free-running trajectory, and two
+    single-context runs agree bit for bit (the fp64 atomic path does not)."""
+    from paper_1101_2678_b200 import aco
+
+    n = 500
+    prob = aco.build_problem(aco.synthetic_instance(n))
+
+    def cfg(nccl_id=None, w=wire):
+        return aco.RunConfig(params=aco.Parameters(m=0, seed=5),
+                             selection=aco.SelectionStrategy(aco.Selection.roulette_full),
+                             deposit=aco.DepositStrategy(aco.Deposit.accumulate), nccl_id=nccl_id,
+                             wire=aco.Wire(w))
+
+    a = aco.Engine(prob, cfg())
+    b = aco.Engine(prob, cfg())
+    c = aco.Engine(prob, cfg(aco.nccl_unique_id()))
+    for it in range(6):
+        ra, rb, rc = a.run_iteration(), b.run_iteration(), c.run_iteration()
+        ta, _ = a.ants()
+        assert np.array_equal(ta, b.ants()[0]) and np.array_equal(ta, c.ants()[0]), it
+        assert ra.best_length == rb.best_length == rc.best_length
+        assert ra.mean_length == rc.mean_length
+        pa = a.pheromone()
+        assert np.array_equal(pa, b.pheromone()), f"run-to-run tau differs at {it}"
+        assert np.array_equal(pa, c.pheromone()), f"sharded tau differs at {it}"
+        assert np.array_equal(a.choice(), c.choice())
+    for e in (a, b, c):
+        e.close()
+
+
+def test_fixed_point_deposit_within_tolerance_of_reference(oracle):
+    """The fixed-point accumulate against deposit_accumulate
+    (pheromone.hpp:195-208) from a shared state: within 1e-5 relative
+    (measured ~1e-15), tours bit-exact."""
+    from paper_1101_2678_b200 import aco
+
+    n = 1002
+    prob = aco.build_problem(aco.synthetic_instance(n))
+    cfg = aco.RunConfig(params=aco.Parameters(m=0, seed=1),
+                        selection=aco.SelectionStrategy(aco.Selection.roulette_full),
+                        deposit=aco.DepositStrategy(aco.Deposit.accumulate), wire=aco.Wire.fixed64)
+    with aco.Engine(prob, cfg) as eng:
+        tau = np.full((n, n), eng.tau0)
+        worst = 0.0
+        for it in range(3):
+            eng.set_pheromone(tau)
+            ch = oracle.choice(prob.dist, tau)
+            eng.run_iteration()
+            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, 0, n)
+            assert np.array_equal(eng.ants()[0], t_ref)
+            tau_ref = oracle.update(tau, t_ref, l_ref, 0.5, 0)
+            rel = float((np.abs(eng.pheromone() - tau_ref) / np.abs(tau_ref)).max())
+            worst = max(worst, rel)
+            tau = tau_ref
+        assert worst <= 1e-12
