@@ -342,3 +342,77 @@ extern "C" int aco_probe_stage(int device, int mode, int warps_per_sm, int steps
     default: return run_stage<6>(device, warps_per_sm, steps, gbps, ms);
     }
 }
+
+// ---------------------------------------------------------------------------
+// Cluster / DSMEM latencies (a thread-block
+// cluster per ant).  One warp per CTA, a cluster of K CTAs on K SMs:
+//   mode 0: DSMEM ping-pong between CTA 0 and CTA 1 (st.shared::cluster into
+//           the peer's flag, spin on the own flag) — cycles per ROUND TRIP;
+//   mode 1: cluster.sync() back to back — cycles per barrier;
+//   mode 2: the per-step exchange a cluster-per-ant roulette needs: every CTA
+//           writes its partial row total into every CTA's slot, one
+//           cluster.sync(), every CTA folds the K partials — cycles per step.
+#include <cooperative_groups.h>
+namespace cgx = cooperative_groups;
+
+template <int K>
+__global__ void __cluster_dims__(K, 1, 1) k_cluster_probe(int mode, int iters, long long* out) {
+    __shared__ volatile unsigned flag;
+    __shared__ double part[16];
+    cgx::cluster_group cl = cgx::this_cluster();
+    const unsigned r = cl.block_rank();
+    if (threadIdx.x == 0) flag = 0;
+    for (int k = threadIdx.x; k < 16; k += 32) part[k] = 0.0;
+    cl.sync();
+    long long t0 = clock64();
+    double acc = 0.0;
+    if (mode == 0) {
+        if (threadIdx.x == 0 && r < 2) {
+            volatile unsigned* peer = cl.map_shared_rank(const_cast<unsigned*>(&flag), r ^ 1u);
+            for (int i = 1; i <= iters; ++i) {
+                if (r == 0) {
+                    *peer = i;
+                    while (flag != static_cast<unsigned>(i)) {}
+                } else {
+                    while (flag != static_cast<unsigned>(i)) {}
+                    *peer = i;
+                }
+            }
+        }
+    } else if (mode == 1) {
+        for (int i = 0; i < iters; ++i) cl.sync();
+    } else {
+        for (int i = 0; i < iters; ++i) {
+            const double mine = static_cast<double>(r + i);
+            if (threadIdx.x < K) {
+                double* dst = cl.map_shared_rank(part, threadIdx.x);
+                dst[(i & 1) * 8 + r] = mine;
+            }
+            cl.sync();
+            double s = 0.0;
+            for (int k = 0; k < K; ++k) s += part[(i & 1) * 8 + k];
+            acc += s;
+        }
+    }
+    const long long t1 = clock64();
+    cl.sync();
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        out[0] = t1 - t0;
+        out[1] = static_cast<long long>(acc);
+    }
+}
+
+extern "C" int aco_probe_cluster(int device, int K, int mode, int iters, double* cycles_per_iter) {
+    cudaSetDevice(device);
+    long long* d = nullptr;
+    cudaMalloc(&d, 2 * sizeof(long long));
+    if (K == 2) k_cluster_probe<2><<<2, 32>>>(mode, iters, d);
+    else if (K == 4) k_cluster_probe<4><<<4, 32>>>(mode, iters, d);
+    else k_cluster_probe<8><<<8, 32>>>(mode, iters, d);
+    long long h[2] = {0, 0};
+    const cudaError_t e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess || cudaGetLastError() != cudaSuccess) return 1;
+    *cycles_per_iter = static_cast<double>(h[0]) / iters;
+    return 0;
+}
