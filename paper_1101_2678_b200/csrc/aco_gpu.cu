@@ -22,7 +22,6 @@
 
 #include "../../include/aco_gpu.h"
 #include "construct.cuh"
-#include "construct_team.cuh"
 #include "host_model.hpp"
 #include "update.cuh"
 
@@ -146,7 +145,6 @@ struct aco_gpu_ctx {
     int rank = 0, world = 1, ant_begin = 0, ant_end = 0, mloc = 0, S = 0;
     int P64 = 0, PW = 0, NV = 0, V = 4, C = 0, R = 1, MAXR = 1, tabu_words = 0;
     int LA = 32;          // lanes sharing a streamed row
-    int team = 1;         // warps per ant (k_construct_team when > 1)
     bool exact_only = false; // k_construct_roulette_exact (rows too long to stream)
     int32_t* host_tours = nullptr; // this construction's streamed host tour buffer (device view)
     double tau0 = 0.0;
@@ -201,6 +199,13 @@ struct aco_gpu_ctx {
     CUdeviceptr mc_uc = 0, mc_va = 0;
     size_t mc_size = 0;
     unsigned long long mc_epoch = 0;
+    // nn + fixed-point accumulate: compact int64 slots + non-list edge records
+    unsigned long long* d_dnn_fix = nullptr;   // n x nn
+    DepositRecord* d_rec = nullptr;            // this rank's records (capacity mloc * n)
+    DepositRecord* d_rec_all = nullptr;        // [world][rec_stride] after the all-gather
+    size_t rec_stride = 0;                     // records per rank in d_rec_all
+    unsigned long long* d_rec_counts = nullptr; // [world]: gathered counts ([rank] = own)
+    unsigned long long* h_rec_counts = nullptr; // pinned copy
     uint8_t* d_qpos = nullptr;          // nn + accumulate: list position of every step's choice
     double* d_dnn = nullptr;            // nn + accumulate: compact n x nn deposit slots
     ncclComm_t comm = nullptr;
@@ -294,63 +299,8 @@ ConstructFn pick_roulette(int NV, int MAXR, bool stream = false) {
     return stream ? pick_roulette_s<WT, true>(NV, MAXR) : pick_roulette_s<WT, false>(NV, MAXR);
 }
 
-template <int K>
-ConstructFn pick_team_k(int NV) {
-    switch (NV) {
-    case 2: return k_construct_team<K, 2>;
-    case 3: return k_construct_team<K, 3>;
-    case 4: return k_construct_team<K, 4>;
-    case 5: return k_construct_team<K, 5>;
-    case 6: return k_construct_team<K, 6>;
-    case 8: return k_construct_team<K, 8>;
-    case 10: return k_construct_team<K, 10>;
-    case 12: return k_construct_team<K, 12>;
-    case 16: return k_construct_team<K, 16>;
-    default: return k_construct_team<K, 20>;
-    }
-}
-ConstructFn pick_team(int K, int NV) {
-    if (K == 2) return pick_team_k<2>(NV);
-    if (K == 4) return pick_team_k<4>(NV);
-    return pick_team_k<8>(NV);
-}
-
-// Warps per ant for the fp32 roulette.  k_construct_team (K = 2/4/8 warps
-// per ant) is bit-exact but measured SLOWER than one warp per ant at every
-// colony size tried, including the latency-bound ones (pr2392, 299 ants:
-// 2.19 ms one warp/ant vs 2.46 / 2.53 / 2.79 ms for K = 2/4/8; pr1002,
-// m = n: 0.82 vs 1.02 ms; profiles/team_sweep_r01.txt): the per-step chain
-// is dominated by the row's L2 round trip and the walk/certification, which
-// a team does not shorten, plus the team's barrier.  So it is opt-in:
-// ACO_TEAM=K (K in {2,4,8}).
-constexpr int kTeamNV[] = {2, 3, 4, 5, 6, 8, 10, 12, 16, 20};
-int choose_team(const aco_gpu_ctx* c) {
-    if (c->cfg.selection != ACO_SEL_ROULETTE || c->stream_kind != ACO_STREAM_FP32) return 1;
-    int K = 1;
-    if (const char* e = std::getenv("ACO_TEAM")) K = std::atoi(e);
-    if (K != 2 && K != 4 && K != 8) return 1;
-    while (K > 1 && K * 32 * 4 * 20 < c->n) K /= 2; // must cover n in K rounds
-    return K;
-}
-
 void choose_stream_layout(aco_gpu_ctx* c) {
     c->V = (c->stream_kind == ACO_STREAM_FP64) ? 2 : 4;
-    c->team = choose_team(c);
-    if (c->team > 1) {
-        c->LA = 32;
-        c->NV = 20;
-        for (int nv : kTeamNV)
-            if (c->team * 32 * 4 * nv >= c->n) {
-                c->NV = nv;
-                break;
-            }
-        c->C = 4 * c->NV;
-        c->R = c->team;
-        c->MAXR = c->team;
-        c->PW = c->R * kLP * c->C;
-        c->tabu_words = c->R * c->C + 4;
-        return;
-    }
     c->LA = 32;
     static const int nvs[] = {2, 4, 8, 12, 16, 19, 20};
     c->NV = 0;
@@ -543,23 +493,6 @@ void launch_construct(aco_gpu_ctx* c) {
         c->construct_desc = "k_construct_roulette_exact grid=" + std::to_string(grid);
         k_construct_roulette_exact<<<grid, 32, smem, c->stream>>>(p, stage_bytes);
         check_launch(c, "k_construct_roulette_exact");
-    } else if (c->cfg.selection == ACO_SEL_ROULETTE && c->team > 1) {
-        ConstructFn fn = pick_team(c->team, c->NV);
-        const size_t smem = 256 + static_cast<size_t>(c->PW) * 4 + smem1 +
-                            static_cast<size_t>((c->n + 31) / 32) * sizeof(double);
-        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * c->team, smem));
-        const int grid = std::max(1, std::min(c->mloc, per_sm * c->num_sms));
-        c->construct_grid = grid;
-        c->construct_desc = "k_construct_team<" + std::to_string(c->team) + "," +
-                            std::to_string(c->NV) + "> grid=" + std::to_string(grid) +
-                            " per_sm=" + std::to_string(per_sm) + " smem=" + std::to_string(smem) +
-                            " row=" + std::to_string(c->PW);
-        if (debug_enabled())
-            std::fprintf(stderr, "construct: %s\n", c->construct_desc.c_str());
-        fn<<<grid, 32 * c->team, smem, c->stream>>>(p);
-        check_launch(c, "k_construct_team");
     } else if (c->cfg.selection == ACO_SEL_ROULETTE) {
         const bool st = c->host_tours != nullptr;
         ConstructFn fn = c->stream_kind == ACO_STREAM_FP64 ? pick_roulette<double>(c->NV, c->MAXR, st)
@@ -860,13 +793,61 @@ void do_construct(aco_gpu_ctx* c) {
 // MULTIMEM, f2 — the deposit's reds go straight to the NVLS multicast object
 // (every GPU's delta at once) and a flag barrier through the same object
 // replaces the collective.
+// nn selection: compact slots + records (k_deposit_nn_fixed), exchanged as
+// 2.4 MB + the records instead of the n^2 delta, applied to the local dense
+// int64 delta by every rank in the same integers.
+void nn_fixed_exchange(aco_gpu_ctx* c, bool shard, const double* inv) {
+    const int grid = c->num_sms * 8;
+    CK(cudaMemsetAsync(c->d_rec_counts + c->rank, 0, sizeof(unsigned long long), c->stream));
+    k_deposit_nn_fixed<<<grid, 256, 0, c->stream>>>(c->d_tours, c->d_qpos, inv, c->n, c->mloc,
+                                                     c->cfg.nn, c->d_stats, c->d_dnn_fix, c->d_rec,
+                                                     c->d_rec_counts + c->rank);
+    check_launch(c, "k_deposit_nn_fixed");
+    const size_t slots = static_cast<size_t>(c->n) * c->cfg.nn;
+    const DepositRecord* rec = c->d_rec;
+    size_t stride = 0;
+    int shards = 1;
+    if (shard) {
+        auto& api = nccl();
+        // every rank's record count (one host round trip sizes the all-gather)
+        NK(api.AllGather(c->d_rec_counts + c->rank, c->d_rec_counts, 1, ncclUint64, c->comm, c->stream));
+        CK(cudaMemcpyAsync(c->h_rec_counts, c->d_rec_counts, c->world * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        unsigned long long mx = 1;
+        for (int g = 0; g < c->world; ++g) mx = std::max(mx, c->h_rec_counts[g]);
+        if (mx > c->rec_stride) { // grow the gather buffer (rare: fallback-heavy colonies)
+            if (c->d_rec_all) CK(cudaFree(c->d_rec_all));
+            c->rec_stride = mx + mx / 4;
+            CK(cudaMalloc(&c->d_rec_all, c->rec_stride * c->world * sizeof(DepositRecord)));
+        }
+        NK(api.GroupStart());
+        NK(api.AllReduce(c->d_dnn_fix, c->d_dnn_fix, slots, ncclUint64, ncclSum, c->comm, c->stream));
+        NK(api.AllGather(c->d_rec, c->d_rec_all, mx * (sizeof(DepositRecord) / 8), ncclUint64, c->comm,
+                         c->stream));
+        NK(api.GroupEnd());
+        rec = c->d_rec_all;
+        stride = mx;
+        shards = c->world;
+    }
+    CK(cudaEventRecord(c->ev[3], c->stream));
+    k_apply_nn_fixed<<<static_cast<int>(std::min<size_t>((slots + 255) / 256, c->num_sms * 16)), 256, 0,
+                       c->stream>>>(c->d_dnn_fix, c->d_nn, c->n, c->cfg.nn, c->P64, c->d_delta_fix);
+    check_launch(c, "k_apply_nn_fixed");
+    k_apply_records<<<grid, 256, 0, c->stream>>>(rec, shard ? c->d_rec_counts : c->d_rec_counts + c->rank,
+                                                  shards, stride, c->P64, c->d_delta_fix);
+    check_launch(c, "k_apply_records");
+}
+
 void do_update_fixed(aco_gpu_ctx* c) {
     const bool shard = c->sharded && !c->external;
     const int shift = c->key_two_stage ? 0 : c->key_shift;
     k_fixed_scale<<<1, 32, 0, c->stream>>>(c->d_stats, c->m, shift, shard ? 1 : 0);
     check_launch(c, "k_fixed_scale");
     const double* inv = c->d_inv + static_cast<size_t>(c->rank) * c->S;
-    if (c->multimem) {
+    if (c->d_dnn_fix) {
+        nn_fixed_exchange(c, shard, inv);
+    } else if (c->multimem) {
         k_deposit_fixed<true><<<c->num_sms * 8, 256, 0, c->stream>>>(
             c->d_tours, inv, c->n, c->P64, c->mloc, c->d_stats,
             reinterpret_cast<unsigned long long*>(c->mc_va));
@@ -888,7 +869,7 @@ void do_update_fixed(aco_gpu_ctx* c) {
                                 c->stream));
         }
     }
-    CK(cudaEventRecord(c->ev[3], c->stream));
+    if (!c->d_dnn_fix) CK(cudaEventRecord(c->ev[3], c->stream));
     launch_rows(c, MODE_DELTA_FIX);
     CK(cudaEventRecord(c->ev[4], c->stream));
     CK(cudaEventRecord(c->ev[5], c->stream));
@@ -1275,7 +1256,22 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         const char* gsplit = std::getenv("ACO_GATHER_SPLIT");
         const bool warp_gather = c->cfg.deposit != ACO_DEP_ACCUMULATE &&
                                  static_cast<size_t>(c->P64) * sizeof(double) + 64 * sizeof(double) <= 32 * 1024;
-        const bool mc_wanted = c->fixed && prm->wire == ACO_WIRE_MULTIMEM && c->world > 1;
+        // nn + fixed: compact slots + records exchange; the dense int64 delta
+        // stays local (no multicast needed — the exchange is already small)
+        const bool nn_fixed = c->fixed && c->cfg.selection == ACO_SEL_NN;
+        const bool mc_wanted = c->fixed && prm->wire == ACO_WIRE_MULTIMEM && c->world > 1 && !nn_fixed;
+        if (nn_fixed) {
+            const size_t ml2 = std::max(1, c->mloc);
+            CK(cudaMalloc(&c->d_qpos, ml2 * n));
+            CK(cudaMemset(c->d_qpos, 255, ml2 * n));
+            const size_t slots = static_cast<size_t>(n) * c->cfg.nn;
+            CK(cudaMalloc(&c->d_dnn_fix, slots * sizeof(unsigned long long)));
+            CK(cudaMemset(c->d_dnn_fix, 0, slots * sizeof(unsigned long long)));
+            CK(cudaMalloc(&c->d_rec, ml2 * n * sizeof(DepositRecord)));
+            CK(cudaMalloc(&c->d_rec_counts, c->world * sizeof(unsigned long long)));
+            CK(cudaMemset(c->d_rec_counts, 0, c->world * sizeof(unsigned long long)));
+            CK(cudaMallocHost(&c->h_rec_counts, c->world * sizeof(unsigned long long)));
+        }
         if (c->fixed && !mc_wanted) { // exact int64 delta (one GPU, or the ncclUint64 all-reduce)
             CK(cudaMalloc(&c->d_delta_fix, cells * sizeof(unsigned long long)));
             CK(cudaMemset(c->d_delta_fix, 0, cells * sizeof(unsigned long long)));
@@ -1368,10 +1364,12 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
     void* bufs[] = {c->d_choice_nn, c->d_choice_nn32, c->d_nn_scale, c->d_topk, c->d_dist, c->d_lut, c->d_etab, c->d_tau, c->d_choice, c->d_choice32,
                     c->d_choice_p64, c->d_scale, c->d_nn, c->d_tours, c->d_len, c->d_inv,
                     c->d_succ, c->d_pred, c->d_delta, c->d_delta32, c->d_stats, c->d_best, c->d_fb, c->d_tourbuf, c->d_verr, c->d_powtab,
-                    c->d_qpos, c->d_dnn, c->d_delta_fix};
+                    c->d_qpos, c->d_dnn, c->d_delta_fix, c->d_dnn_fix, c->d_rec, c->d_rec_all,
+                    c->d_rec_counts};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_stats) cudaFreeHost(c->h_stats);
+    if (c->h_rec_counts) cudaFreeHost(c->h_rec_counts);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -1477,7 +1475,7 @@ aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* to
         // device-mapped tours_out while it is built (TourStream); otherwise
         // the tours are copied after the construction.
         c->host_tours = nullptr;
-        if (tours_out && c->cfg.selection == ACO_SEL_ROULETTE && !c->exact_only && c->team == 1 &&
+        if (tours_out && c->cfg.selection == ACO_SEL_ROULETTE && !c->exact_only &&
             c->mloc > 0) {
             cudaPointerAttributes at{};
             if (cudaPointerGetAttributes(&at, tours_out) == cudaSuccess &&

@@ -40,12 +40,6 @@
 #ifndef ACO_LDG
 #define ACO_LDG 2 // 1: ld.global.nc.L1::no_allocate; 2: ld.global.nc (L1-allocating)
 #endif
-#ifndef ACO_ROW_SRC
-#define ACO_ROW_SRC 0 // fp32 single-round roulette: 0 = TMA row staging, 1 = L1-allocating LDG
-#endif
-#ifndef ACO_GROUPWALK
-#define ACO_GROUPWALK 1 // fp32 single-round roulette: 1 = group walk, 0 = quad-scan walk
-#endif
 #ifndef ACO_TIMING
 #define ACO_TIMING 0 // per-phase clock64() accounting into ConstructParams::timing
 #endif
@@ -553,8 +547,8 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
     constexpr int GE = GV * V;                         // cities per group
     constexpr int D1 = ceil_log2<GE>() + ceil_log2<NG>();
     constexpr bool F32 = sizeof(WT) == 4;
-    constexpr bool kLDG = (ACO_ROW_SRC == 1) && F32 && MAXR == 1; // rows via L1, not smem
-    constexpr bool kGroupWalk = (ACO_GROUPWALK == 1) && F32 && MAXR == 1 && !kLDG;
+    // fp32 single-round rows: the group walk; otherwise the quad-scan walk
+    constexpr bool kGroupWalk = F32 && MAXR == 1;
     static_assert(GE <= 32 && 32 % GE == 0, "a group's bits live in one window word");
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -611,7 +605,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
 
         for (int step = 1; step < n; ++step) {
             const WT* __restrict__ grow = wbase + static_cast<size_t>(cur) * p.PW;
-            if (!kLDG && !prefetched && lane == 0) {
+            if (!prefetched && lane == 0) {
                 fence_proxy_async_smem(); // generic reads of buf happen-before the refill
                 mbar_expect_tx(bar, row_bytes);
                 tma_row(buf, grow, row_bytes, bar);
@@ -623,12 +617,10 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
             const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
             const float u32 = __double2float_rn(u);
             __syncwarp();
-            if (!kLDG) {
-                mbar_wait(bar, phase);
-                phase ^= 1u;
-            }
+            mbar_wait(bar, phase);
+            phase ^= 1u;
             prefetched = false;
-            const WT* rowsrc = kLDG ? grow : buf; // where this step reads the row
+            const WT* rowsrc = buf; // the staged row
             TICK(6);
 
             AT incl[MAXR];
@@ -656,8 +648,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                             const int tv = g * GV + tt;
                             VT v;
                             if (tv < NV) {
-                                if constexpr (kLDG) v = __ldg(rv + tv * kLP);
-                                else v = rv[tv * kLP];
+                                v = rv[tv * kLP];
                             } else {
                                 if constexpr (F32) v = make_float4(0.f, 0.f, 0.f, 0.f);
                                 else v = make_double2(0.0, 0.0);
@@ -823,9 +814,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                         if constexpr (F32) {
                             const float4* qp = reinterpret_cast<const float4*>(
                                 rowsrc + rs * kLP * C + (ql * kLP + L) * 4);
-                            float4 v;
-                            if constexpr (kLDG) v = __ldg(qp);
-                            else v = *qp;
+                            const float4 v = *qp;
                             xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
                         } else {
                             const double2 v0 = *reinterpret_cast<const double2*>(
@@ -881,7 +870,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                 TICK(2);
                 // speculative refill, issued by the certifying lane itself: every
                 // read of buf in this step has returned (its value fed the ballots)
-                if (!kLDG && cert && step + 1 < n) {
+                if (cert && step + 1 < n) {
                     mbar_expect_tx(bar, row_bytes);
                     tma_row(buf, wbase + static_cast<size_t>(J) * p.PW, row_bytes, bar);
                 }
@@ -889,26 +878,10 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
                 ok = cb != 0u;
                 if (ok) {
                     next = __shfl_sync(kFull, J, __ffs(cb) - 1);
-                    prefetched = !kLDG && step + 1 < n;
-                    if (kLDG && step + 1 < n) { // speculative L1 prefetch of the next row
-                        const char* nr = reinterpret_cast<const char*>(wbase + static_cast<size_t>(next) * p.PW);
-                        for (int ln = lane; ln * 128 < static_cast<int>(row_bytes); ln += 32)
-                            asm volatile("prefetch.global.L1 [%0];" ::"l"(nr + ln * 128));
-                    }
+                    prefetched = step + 1 < n;
                 }
             }
             TICK(3);
-            if (kLDG && !ok) { // tier 2 reads the row from smem: stage it now
-                __syncwarp();
-                if (lane == 0) {
-                    fence_proxy_async_smem();
-                    mbar_expect_tx(bar, row_bytes);
-                    tma_row(buf, grow, row_bytes, bar);
-                }
-                __syncwarp();
-                mbar_wait(bar, phase);
-                phase ^= 1u;
-            }
             if (!ok) { // middle tier: fp64 sums over the fp32 row still in smem
                 const int j2 = certify_fp64<WT, NV, MAXR>(buf, tabu, n, p.R, u, lane);
                 if (j2 >= 0) {

@@ -377,6 +377,73 @@ __global__ void k_deposit_fixed(const int32_t* __restrict__ tours, const double*
     }
 }
 
+// nn selection with the fixed-point accumulate (config 5, any G): list edges
+// add round(w_k 2^s) to the compact int64 slots dnn[a][q]; every other edge
+// (argmax fallbacks, the closing edge) is appended to a record list
+// {a, b, round(w_k 2^s)}.  Sharded, only the compact slots (n x nn x 8 B,
+// 2.4 MB at 10k) are all-reduced and the records all-gathered — instead of
+// the n^2 delta (800 MB) — and every rank scatters the same integers into its
+// local dense delta (k_apply_nn_fixed, k_apply_records): exact sums, so tau is
+// bit-identical on every rank and for every G.
+struct __align__(16) DepositRecord {
+    int32_t a, b;
+    unsigned long long v;
+};
+
+__global__ void k_deposit_nn_fixed(const int32_t* __restrict__ tours, const uint8_t* __restrict__ qpos,
+                                   const double* __restrict__ inv, int n, int mloc, int nn,
+                                   const long long* __restrict__ stats,
+                                   unsigned long long* __restrict__ dnn, DepositRecord* __restrict__ rec,
+                                   unsigned long long* __restrict__ rec_count) {
+    const int sh = static_cast<int>(stats[7]);
+    if (sh < 0) return;
+    const size_t total = static_cast<size_t>(mloc) * n;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int kl = static_cast<int>(i / n), s = static_cast<int>(i - static_cast<size_t>(kl) * n);
+        const int32_t* t = tours + static_cast<size_t>(kl) * (n + 1);
+        const int a = t[s];
+        const int q = qpos[i];
+        const unsigned long long v = __double2ull_rn(scalbn(inv[kl], sh));
+        if (q < nn) {
+            atomicAdd(dnn + static_cast<size_t>(a) * nn + q, v);
+        } else {
+            const unsigned long long at = atomicAdd(rec_count, 1ull);
+            rec[at] = DepositRecord{a, t[s + 1], v};
+        }
+    }
+}
+
+__global__ void k_apply_nn_fixed(unsigned long long* __restrict__ dnn, const int32_t* __restrict__ nn_lists,
+                                 int n, int nn, int P64, unsigned long long* __restrict__ delta) {
+    const size_t slots = static_cast<size_t>(n) * nn;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < slots;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const unsigned long long d = dnn[i];
+        if (d != 0ull) {
+            const int a = static_cast<int>(i / nn), b = nn_lists[i];
+            atomicAdd(delta + static_cast<size_t>(a) * P64 + b, d);
+            atomicAdd(delta + static_cast<size_t>(b) * P64 + a, d);
+            dnn[i] = 0ull;
+        }
+    }
+}
+
+// records of `shards` ranks, rank g's at rec[g * stride], counts[g] of them
+__global__ void k_apply_records(const DepositRecord* __restrict__ rec, const unsigned long long* __restrict__ counts,
+                                int shards, size_t stride, int P64, unsigned long long* __restrict__ delta) {
+    for (int g = 0; g < shards; ++g) {
+        const size_t cnt = counts[g];
+        const DepositRecord* r = rec + static_cast<size_t>(g) * stride;
+        for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < cnt;
+             i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+            const DepositRecord e = r[i];
+            atomicAdd(delta + static_cast<size_t>(e.a) * P64 + e.b, e.v);
+            atomicAdd(delta + static_cast<size_t>(e.b) * P64 + e.a, e.v);
+        }
+    }
+}
+
 // Cross-GPU barrier over the multicast object (ACO_WIRE_MULTIMEM), one
 // thread: make this GPU's reds visible system-wide, add 1 to every GPU's copy
 // of the flag with one release red through the switch, then wait until the

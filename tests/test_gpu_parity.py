@@ -214,45 +214,6 @@ def test_att48_trace(aco, golden):
     assert best == g["trace_roulette_accumulate"]["best"]
 
 
-@pytest.mark.parametrize("K", ["1", "2", "4", "8"])
-def test_team_construction_bit_exact(aco, oracle, monkeypatch, K):
-    """k_construct_team (K warps per ant) and the one-warp kernel (K=1) give
-    the reference's tours over several iterations of the gather path."""
-    monkeypatch.setenv("ACO_TEAM", K)
-    n = 1002
-    prob, eng = make(aco, n, deposit=1)
-    with eng:
-        tau = np.full((n, n), eng.tau0)
-        for it in range(2):
-            ch = oracle.choice(prob.dist, tau)
-            eng.run_iteration()
-            if K != "1":
-                assert f"k_construct_team<{K}," in eng.describe()
-            else:
-                assert "k_construct_roulette<" in eng.describe()
-            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, 0, n)
-            t, l = eng.ants()
-            assert np.array_equal(t, t_ref), f"iteration {it}"
-            assert np.array_equal(l, l_ref)
-            tau = oracle.update(tau, t_ref, l_ref, 0.5, 1)
-            assert np.array_equal(eng.pheromone(), tau)
-
-
-@pytest.mark.parametrize("K", ["2", "8"])
-def test_team_construction_pr2392_subset(aco, oracle, monkeypatch, K):
-    monkeypatch.setenv("ACO_TEAM", K)
-    n = 2392
-    prob, eng = make(aco, n, ant_range=(700, 764))
-    with eng:
-        eng.construct()
-        assert f"k_construct_team<{K}," in eng.describe()
-        t, l = eng.ants()
-        tau = np.full((n, n), eng.tau0)
-        t_ref, l_ref, _ = oracle.construct(prob.dist, oracle.choice(prob.dist, tau), 1, 0, 700, 764)
-        assert np.array_equal(t, t_ref)
-        assert np.array_equal(l, l_ref)
-
-
 @pytest.mark.parametrize("topk", ["1", "0"])
 def test_nn_argmax_cache_bit_exact(aco, oracle, monkeypatch, topk):
     """The nn selection's argmax fallback through the per-row top-K cache

@@ -136,23 +136,25 @@ def test_nccl_exchange_path_one_rank(deposit, wire):
     nccl.close()
 
 
-@pytest.mark.parametrize("wire", [2, 3])
-def test_fixed_point_exchange_bit_identical_for_any_world(wire):
+@pytest.mark.parametrize("wire,selection", [(2, 0), (3, 0), (2, 1), (3, 1)])
+def test_fixed_point_exchange_bit_identical_for_any_world(wire, selection):
     """ACO_WIRE_FIXED64 / MULTIMEM: every deposit is an exact int64
     fixed-point sum, so tau does not depend on the order of the reds or on
     the exchange.  The sharded protocol on a one-rank NCCL communicator
     (ncclUint64 all-reduce; MULTIMEM at world 1 runs the same FIXED64 path —
     its multicast object needs >= 2 GPUs) reproduces the single-context
     fixed-point colony BIT FOR BIT over a free-running trajectory, and two
-    single-context runs agree bit for bit (the fp64 atomic path does not)."""
+    single-context runs agree bit for bit (the fp64 atomic path does not).
+    nn selection (nn = 8: frequent argmax fallbacks) runs the compact-slot +
+    record exchange (count all-gather, record all-gather, slot all-reduce)."""
     from paper_1101_2678_b200 import aco
 
     n = 500
     prob = aco.build_problem(aco.synthetic_instance(n))
 
     def cfg(nccl_id=None, w=wire):
-        return aco.RunConfig(params=aco.Parameters(m=0, seed=5),
-                             selection=aco.SelectionStrategy(aco.Selection.roulette_full),
+        return aco.RunConfig(params=aco.Parameters(m=0, seed=5, nn=8),
+                             selection=aco.SelectionStrategy(aco.Selection(selection)),
                              deposit=aco.DepositStrategy(aco.Deposit.accumulate), nccl_id=nccl_id,
                              wire=aco.Wire(w))
 
@@ -173,16 +175,19 @@ def test_fixed_point_exchange_bit_identical_for_any_world(wire):
         e.close()
 
 
-def test_fixed_point_deposit_within_tolerance_of_reference(oracle):
+@pytest.mark.parametrize("selection", [0, 1])
+def test_fixed_point_deposit_within_tolerance_of_reference(oracle, selection):
     """The fixed-point accumulate against deposit_accumulate
     (pheromone.hpp:195-208) from a shared state: within 1e-5 relative
-    (measured ~1e-15), tours bit-exact."""
+    (measured ~1e-15), tours bit-exact; nn selection through the compact
+    slots + records."""
     from paper_1101_2678_b200 import aco
 
     n = 1002
     prob = aco.build_problem(aco.synthetic_instance(n))
-    cfg = aco.RunConfig(params=aco.Parameters(m=0, seed=1),
-                        selection=aco.SelectionStrategy(aco.Selection.roulette_full),
+    nnl = oracle.nn_lists(prob.dist, 10)
+    cfg = aco.RunConfig(params=aco.Parameters(m=0, seed=1, nn=10),
+                        selection=aco.SelectionStrategy(aco.Selection(selection)),
                         deposit=aco.DepositStrategy(aco.Deposit.accumulate), wire=aco.Wire.fixed64)
     with aco.Engine(prob, cfg) as eng:
         tau = np.full((n, n), eng.tau0)
@@ -191,7 +196,8 @@ def test_fixed_point_deposit_within_tolerance_of_reference(oracle):
             eng.set_pheromone(tau)
             ch = oracle.choice(prob.dist, tau)
             eng.run_iteration()
-            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, 0, n)
+            t_ref, l_ref, _ = oracle.construct(prob.dist, ch, 1, it, 0, n, selection=selection,
+                                               nn_lists=nnl if selection else None)
             assert np.array_equal(eng.ants()[0], t_ref)
             tau_ref = oracle.update(tau, t_ref, l_ref, 0.5, 0)
             rel = float((np.abs(eng.pheromone() - tau_ref) / np.abs(tau_ref)).max())
