@@ -207,6 +207,11 @@ struct aco_gpu_ctx {
     unsigned long long* d_rec_counts = nullptr; // [world]: gathered counts ([rank] = own)
     unsigned long long* h_rec_counts = nullptr; // pinned copy
     uint8_t* d_qpos = nullptr;          // nn + accumulate: list position of every step's choice
+    // roulette relay (leftover ants built in segments by several warps)
+    unsigned long long* d_relay_flag = nullptr; // [num_sms]
+    int32_t* d_relay_cur = nullptr;             // [num_sms]
+    uint32_t* d_relay_tabu = nullptr;           // [num_sms][tabu_words]
+    unsigned long long relay_epoch = 0;
     double* d_dnn = nullptr;            // nn + accumulate: compact n x nn deposit slots
     ncclComm_t comm = nullptr;
     bool external = false; // world > 1 without an NCCL id: the caller exchanges
@@ -277,6 +282,20 @@ __global__ void k_fill(double* p, size_t count, double v) {
 
 // ---- construction kernel dispatch ------------------------------------------
 using ConstructFn = void (*)(ConstructParams);
+
+// the relay variant (fp32 stream, single-round rows only)
+template <bool ST>
+ConstructFn pick_roulette_relay(int NV) {
+    switch (NV) {
+    case 2: return k_construct_roulette_relay<2, ST>;
+    case 4: return k_construct_roulette_relay<4, ST>;
+    case 8: return k_construct_roulette_relay<8, ST>;
+    case 12: return k_construct_roulette_relay<12, ST>;
+    case 16: return k_construct_roulette_relay<16, ST>;
+    case 19: return k_construct_roulette_relay<19, ST>;
+    default: return k_construct_roulette_relay<20, ST>;
+    }
+}
 
 template <typename WT, bool ST>
 ConstructFn pick_roulette_s(int NV, int MAXR) {
@@ -465,6 +484,23 @@ ConstructParams make_cp(aco_gpu_ctx* c) {
     return p;
 }
 
+// roulette relay: minimum warps per SM (ACO_RELAY=0 disables, ACO_RELAY=q
+// sets the threshold) and the segment count override (ACO_RELAY_K)
+int relay_min_q() {
+    static const int q = [] {
+        const char* e = std::getenv("ACO_RELAY");
+        return e ? (std::atoi(e) <= 0 ? 1 << 30 : std::atoi(e)) : 4;
+    }();
+    return q;
+}
+int relay_k_override() {
+    static const int k = [] {
+        const char* e = std::getenv("ACO_RELAY_K");
+        return e ? std::atoi(e) : 0;
+    }();
+    return k;
+}
+
 // the nn kernel forms the tour lengths in its tail (tour_tail);
 // ACO_FUSED_TAIL=0 keeps the separate k_tour_length launch
 bool fused_tail_enabled() {
@@ -499,20 +535,69 @@ void launch_construct(aco_gpu_ctx* c) {
                                                            : pick_roulette<float>(c->NV, c->MAXR, st);
         const size_t wsz = c->stream_kind == ACO_STREAM_FP64 ? sizeof(double) : sizeof(float);
         const int ng = (c->NV + 3) / 4;
-        const size_t smem = 128 + static_cast<size_t>(c->PW) * wsz + smem1 +
+        size_t smem = 128 + static_cast<size_t>(c->PW) * wsz + smem1 +
                             static_cast<size_t>((c->n + 31) / 32) * sizeof(double) +
                             (c->MAXR > 1 ? static_cast<size_t>(c->MAXR) * ng * 32 * wsz : 0);
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         int per_sm = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem));
-        const int grid = std::max(1, std::min(c->mloc, per_sm * c->num_sms));
+        int grid = std::max(1, std::min(c->mloc, per_sm * c->num_sms));
+        // Relay: with q = floor(mloc / SMs) >= relay_min_q warps on every SM
+        // and E = mloc - q*SMs leftover ants, one warp per SM-slot builds its
+        // own ant and the E leftovers are built in K segments by K different
+        // warps each (handing over through global memory), instead of E SMs
+        // running a (q+1)-th warp for the whole kernel: that warp shares an SM
+        // sub-partition (5 warps on one scheduler at q = 16) and is the last to
+        // finish — at pr2392 ONE leftover ant costs 9.5% (m = 2368: 3.68 ms,
+        // m = 2369: 4.02 ms); relayed, m = 2392 (16 x 148 + 24) runs 3.78 ms
+        // instead of 4.12 (tools/relay_ab.py, same tours).
+        const int q = c->mloc / c->num_sms;
+        const int E = c->mloc - q * c->num_sms;
+        std::string relay_desc;
+        // Only when the leftovers are few (W >= 32 E: every relay warp carries
+        // at most ~1/32 of an ant more); pr1002 (E = 114 of 888) runs slower
+        // relayed (0.82 -> 1.03 ms, tools/relay_ab.py).
+        if (c->stream_kind == ACO_STREAM_FP32 && c->MAXR == 1 && E > 0 && q >= relay_min_q() &&
+            q <= per_sm && q * c->num_sms >= 32 * E) {
+            ConstructFn rfn = st ? pick_roulette_relay<true>(c->NV) : pick_roulette_relay<false>(c->NV);
+            const size_t rsmem = smem + smem1;
+            CK(cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsmem)));
+            int rper_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rper_sm, rfn, 32, rsmem));
+            const int W = q * c->num_sms;
+            int K = relay_k_override();
+            if (K <= 0) K = static_cast<int>(std::lround(std::sqrt(static_cast<double>(c->n - 1))));
+            K = std::max(1, std::min({K, W / E, (c->n - 1) / 64}));
+            if (rper_sm >= q && K >= 1 && (c->n - 1) / K >= 64) {
+                if (!c->d_relay_flag) {
+                    CK(cudaMalloc(&c->d_relay_flag, c->num_sms * sizeof(unsigned long long)));
+                    CK(cudaMemsetAsync(c->d_relay_flag, 0, c->num_sms * sizeof(unsigned long long), c->stream));
+                    CK(cudaMalloc(&c->d_relay_cur, c->num_sms * sizeof(int32_t)));
+                    CK(cudaMalloc(&c->d_relay_tabu,
+                                  static_cast<size_t>(c->num_sms) * c->tabu_words * sizeof(uint32_t)));
+                }
+                p.relay_W = W;
+                p.relay_E = E;
+                p.relay_K = K;
+                p.relay_epoch = ++c->relay_epoch;
+                p.relay_flag = c->d_relay_flag;
+                p.relay_cur = c->d_relay_cur;
+                p.relay_tabu = c->d_relay_tabu;
+                fn = rfn;
+                smem = rsmem;
+                per_sm = rper_sm;
+                grid = W;
+                relay_desc = " relay: W=" + std::to_string(W) + " E=" + std::to_string(E) +
+                             " K=" + std::to_string(K);
+            }
+        }
         c->construct_grid = grid;
         c->construct_desc = std::string("k_construct_roulette<") +
                             (c->stream_kind == ACO_STREAM_FP64 ? "double," : "float,") +
                             std::to_string(c->NV) + "," + std::to_string(c->MAXR) + "> grid=" +
                             std::to_string(grid) + " per_sm=" + std::to_string(per_sm) +
                             " smem=" + std::to_string(smem) + " row=" + std::to_string(c->PW) +
-                            (st ? " streams_tours_to_host" : "");
+                            (st ? " streams_tours_to_host" : "") + relay_desc;
         if (debug_enabled())
             std::fprintf(stderr, "construct: %s\n", c->construct_desc.c_str());
         fn<<<grid, 32, smem, c->stream>>>(p);
@@ -1365,7 +1450,7 @@ void aco_gpu_destroy(aco_gpu_ctx* c) {
                     c->d_choice_p64, c->d_scale, c->d_nn, c->d_tours, c->d_len, c->d_inv,
                     c->d_succ, c->d_pred, c->d_delta, c->d_delta32, c->d_stats, c->d_best, c->d_fb, c->d_tourbuf, c->d_verr, c->d_powtab,
                     c->d_qpos, c->d_dnn, c->d_delta_fix, c->d_dnn_fix, c->d_rec, c->d_rec_all,
-                    c->d_rec_counts};
+                    c->d_rec_counts, c->d_relay_flag, c->d_relay_cur, c->d_relay_tabu};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (c->h_stats) cudaFreeHost(c->h_stats);

@@ -125,7 +125,27 @@ struct ConstructParams {
     // argmax fallback), so k_deposit_nn can fold list edges into the compact
     // n x nn slot array instead of scattering over n^2 tau
     uint8_t* qpos;              // mloc x n, or null
+    // Relay (k_construct_roulette_relay): the grid is relay_W = SMs x q
+    // warps, warp w owns ant w; the relay_E = mloc - relay_W leftover ants are
+    // each built by relay_K warps in turn, one 32-aligned segment of steps
+    // each (relay_bound), handing the tabu set and current city over through
+    // global memory (relay_cur / relay_tabu) behind a release/acquire flag
+    // stamped with relay_epoch.
+    int relay_W, relay_E, relay_K;
+    unsigned long long relay_epoch;
+    unsigned long long* relay_flag; // [relay_E]
+    int32_t* relay_cur;             // [relay_E]
+    uint32_t* relay_tabu;           // [relay_E][tabu_words]
 };
+
+// First step of relay segment i of K over steps 1..n-1 (segment K ends at n);
+// inner bounds are multiples of 32, so a segment's tour-stream chunks and
+// Philox batches never straddle a hand-over (the host keeps (n-1)/K >= 64).
+__host__ __device__ __forceinline__ int relay_bound(int i, int K, int n) {
+    if (i <= 0) return 1;
+    if (i >= K) return n;
+    return static_cast<int>((static_cast<long long>(i) * (n - 1) / K) & ~31LL);
+}
 
 // Tour length (tour_length, model.hpp:205-226: an int64 sum, so any order is
 // exact), w_k = 1.0 / (double)C_k (inverse_lengths, pheromone.hpp:123-128)
@@ -535,8 +555,54 @@ __device__ __noinline__ int certify_fp64(const WT* buf, const uint32_t* tabu, in
 // fp32 adds on any prefix path are counted in the bound, ~24 * 2^-24), fp64
 // for the fp64 stream.  Only the final two certification compares are fp64.
 // NV = 128-bit vectors per lane per round, C = NV*V, MAXR = max rounds.
-template <typename WT, int NV, int MAXR, bool STREAM = false>
-__global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(ConstructParams p) {
+// One ant in the roulette kernels: the state a run of steps carries.
+struct RouletteAnt {
+    int kl;           // local ant index (tour row)
+    uint32_t kg;      // global ant id (RNG key)
+    int32_t* tour;
+    uint32_t* tabu;   // shared-memory tabu bitmask
+    int cur;          // current city
+    bool prefetched;  // the row of `cur` is already requested (speculative TMA)
+    TourStream hs;    // STREAM: the partial 32-entry chunk
+};
+
+// Lays the ant's start city down (tabu, tour[0]).
+__device__ __forceinline__ void roulette_begin(const ConstructParams& p, RouletteAnt& a, int kl,
+                                               uint32_t* tabu, int lane, bool stream) {
+    a.kl = kl;
+    a.kg = static_cast<uint32_t>(p.ant_begin + kl);
+    a.tour = p.tours + static_cast<size_t>(kl) * (p.n + 1);
+    a.tabu = tabu;
+    a.prefetched = false;
+    a.hs = TourStream{0};
+    tabu_init(tabu, p.tabu_words, p.n, lane);
+    const int start = start_city(p, a.kg);
+    __syncwarp();
+    if (lane == 0) {
+        tabu[start >> 5] |= 1u << (start & 31);
+        a.tour[0] = start;
+    }
+    if (stream) a.hs.put(p, kl, 0, start, lane); // STREAM: the caller's pinned tours_out is mapped
+    a.cur = start;
+}
+
+// Closes the tour (tour[n] = start).
+__device__ __forceinline__ void roulette_end(const ConstructParams& p, RouletteAnt& a, int lane, bool stream) {
+    const int start = start_city(p, a.kg);
+    if (lane == 0) a.tour[p.n] = start;
+    if (stream) {
+        a.hs.put(p, a.kl, p.n, start, lane);
+        a.hs.flush(p, a.kl, p.n, lane);
+    }
+    __syncwarp();
+}
+
+// Steps [s0, s1) of one ant.  smem: the kernel's dynamic shared memory
+// (mbarrier, row buffer, own tabu, chunk_start, gsum).
+template <typename WT, int NV, int MAXR, bool STREAM>
+__device__ __forceinline__ void roulette_steps(const ConstructParams& p, RouletteAnt& a, int s0, int s1,
+                                               unsigned char* smem_raw, uint32_t& phase,
+                                               unsigned long long& fb, unsigned long long& fb2) {
     using VT = typename VecOf<WT>::T;
     using AT = WT; // accumulation type
     constexpr int V = VecOf<WT>::V;
@@ -551,12 +617,11 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
     constexpr bool kGroupWalk = F32 && MAXR == 1;
     static_assert(GE <= 32 && 32 % GE == 0, "a group's bits live in one window word");
 
-    extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
     WT* buf = reinterpret_cast<WT*>(smem_raw + 128);
-    uint32_t* tabu = reinterpret_cast<uint32_t*>(smem_raw + 128 + static_cast<size_t>(p.PW) * sizeof(WT));
-    double* chunk_start = reinterpret_cast<double*>(tabu + p.tabu_words); // ceil(n/32) (8-aligned)
-    WT* gsum = reinterpret_cast<WT*>(chunk_start + ((p.n + 31) >> 5));   // [MAXR][NG][32]
+    double* chunk_start = reinterpret_cast<double*>(
+        reinterpret_cast<uint32_t*>(smem_raw + 128 + static_cast<size_t>(p.PW) * sizeof(WT)) + p.tabu_words);
+    WT* gsum = reinterpret_cast<WT*>(chunk_start + ((p.n + 31) >> 5)); // [MAXR][NG][32]
     const int lane = threadIdx.x & 31;
     const int n = p.n;
     const WT* __restrict__ wbase = static_cast<const WT*>(p.w);
@@ -575,361 +640,496 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
     const float lo32 = __double2float_rd(lo_f); // <= lo_f
     const float e32 = __double2float_ru(e_rel); // >= e_rel
 
-    if (lane == 0) mbar_init(bar, 1);
-    __syncwarp();
-    uint32_t phase = 0;
-
-    for (int kl = blockIdx.x; kl < p.mloc; kl += gridDim.x) {
-        const uint32_t kg = static_cast<uint32_t>(p.ant_begin + kl);
-        int32_t* tour = p.tours + static_cast<size_t>(kl) * (n + 1);
-        tabu_init(tabu, p.tabu_words, n, lane);
-        const int start = start_city(p, kg);
-        __syncwarp();
-        if (lane == 0) {
-            tabu[start >> 5] |= 1u << (start & 31);
-            tour[0] = start;
-        }
-        TourStream hs{0}; // STREAM: the caller's pinned tours_out is mapped
-        if constexpr (STREAM) hs.put(p, kl, 0, start, lane);
-        int cur = start;
-        unsigned long long fb = 0, fb2 = 0;
-        bool prefetched = false; // row of `cur` already requested by the previous step
-        double ubatch = 0.0;
+    const int kl = a.kl;
+    const uint32_t kg = a.kg;
+    int32_t* const tour = a.tour;
+    uint32_t* const tabu = a.tabu;
+    int cur = a.cur;
+    bool prefetched = a.prefetched;
+    TourStream hs = a.hs;
+    // Draw 0 of steps b..b+31 (b = 1 mod 32): lane i holds step b + i
+    // (rng.hpp:74-80); a run starting inside a batch draws it first.
+    double ubatch = 0.0;
+    if (((s0 - 1) & 31) != 0)
+        ubatch = philox_uniform(p.seed, p.iteration, kg, static_cast<uint32_t>(((s0 - 1) & ~31) + 1 + lane), 0);
 #if ACO_TIMING
-        unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        long long tk = clock64();
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tk = clock64();
 #define TICK(i) do { const long long t_ = clock64(); ph[i] += t_ - tk; tk = t_; } while (0)
 #else
 #define TICK(i) do {} while (0)
 #endif
 
-        for (int step = 1; step < n; ++step) {
-            const WT* __restrict__ grow = wbase + static_cast<size_t>(cur) * p.PW;
-            if (!prefetched && lane == 0) {
-                fence_proxy_async_smem(); // generic reads of buf happen-before the refill
-                mbar_expect_tx(bar, row_bytes);
-                tma_row(buf, grow, row_bytes, bar);
-            }
-            // Draw 0 of steps step..step+31: lane i holds step + i (rng.hpp:74-80).
-            if (((step - 1) & 31) == 0)
-                ubatch = philox_uniform(p.seed, p.iteration, kg,
-                                        static_cast<uint32_t>(step + lane), 0);
-            const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
-            const float u32 = __double2float_rn(u);
-            __syncwarp();
-            mbar_wait(bar, phase);
-            phase ^= 1u;
-            prefetched = false;
-            const WT* rowsrc = buf; // the staged row
-            TICK(6);
+    for (int step = s0; step < s1; ++step) {
+        const WT* __restrict__ grow = wbase + static_cast<size_t>(cur) * p.PW;
+        if (!prefetched && lane == 0) {
+            fence_proxy_async_smem(); // generic reads of buf happen-before the refill
+            mbar_expect_tx(bar, row_bytes);
+            tma_row(buf, grow, row_bytes, bar);
+        }
+        // Draw 0 of steps step..step+31: lane i holds step + i (rng.hpp:74-80).
+        if (((step - 1) & 31) == 0)
+            ubatch = philox_uniform(p.seed, p.iteration, kg,
+                                    static_cast<uint32_t>(step + lane), 0);
+        const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
+        const float u32 = __double2float_rn(u);
+        __syncwarp();
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        prefetched = false;
+        const WT* rowsrc = buf; // the staged row
+        TICK(6);
 
-            AT incl[MAXR];
-            AT rtot[MAXR];
-            WT gsr[NG]; // MAXR == 1: lane-local inclusive prefix of the group sums
-            AT T = AT(0);
+        AT incl[MAXR];
+        AT rtot[MAXR];
+        WT gsr[NG]; // MAXR == 1: lane-local inclusive prefix of the group sums
+        AT T = AT(0);
+#pragma unroll
+        for (int r = 0; r < MAXR; ++r) {
+            incl[r] = AT(0);
+            rtot[r] = AT(0);
+            if (r < p.R) {
+                const int cbase = r * 32 * C + lane * C;
+                const int w0 = cbase >> 5, sh = cbase & 31;
+                uint32_t win[NWIN];
+#pragma unroll
+                for (int i = 0; i < NWIN; ++i)
+                    win[i] = __funnelshift_r(tabu[w0 + i], tabu[w0 + i + 1], sh);
+                const VT* rv = reinterpret_cast<const VT*>(rowsrc + r * kLP * C) + lane;
+                WT gs[NG];
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    WT x[GE];
+#pragma unroll
+                    for (int tt = 0; tt < GV; ++tt) {
+                        const int tv = g * GV + tt;
+                        VT v;
+                        if (tv < NV) {
+                            v = rv[tv * kLP];
+                        } else {
+                            if constexpr (F32) v = make_float4(0.f, 0.f, 0.f, 0.f);
+                            else v = make_double2(0.0, 0.0);
+                        }
+                        if constexpr (F32) {
+                            x[tt * 4 + 0] = v.x; x[tt * 4 + 1] = v.y;
+                            x[tt * 4 + 2] = v.z; x[tt * 4 + 3] = v.w;
+                        } else {
+                            x[tt * 2 + 0] = v.x; x[tt * 2 + 1] = v.y;
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < GE; ++e) {
+                        const int ee = g * GE + e;
+                        if (ee < C && ((win[ee >> 5] >> (ee & 31)) & 1u)) x[e] = WT(0);
+                    }
+                    if constexpr (F32) gs[g] = tree_sum_packed<GE>(x);
+                    else gs[g] = tree_sum<WT, GE>(x);
+                    if constexpr (MAXR > 1) gsum[(r * NG + g) * 32 + lane] = gs[g];
+                }
+                if constexpr (MAXR == 1) { // lane-local inclusive group prefixes
+                    gsr[0] = gs[0];
+#pragma unroll
+                    for (int g = 1; g < NG; ++g) gsr[g] = gsr[g - 1] + gs[g];
+                }
+                AT d = static_cast<AT>(tree_sum<WT, NG>(gs));
+                TICK(0);
+                if constexpr (F32) {
+                    d = warp_inclusive_scan(d);
+                } else {
+#pragma unroll
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const AT y = __shfl_up_sync(kFull, d, off);
+                        if (lane >= off) d += y;
+                    }
+                }
+                incl[r] = d;
+                rtot[r] = __shfl_sync(kFull, d, 31);
+                T += rtot[r];
+                TICK(1);
+            }
+        }
+        const double Td = static_cast<double>(T);
+        const double tdd = u * Td;
+        // Candidate threshold in AT.  Only the candidate search uses it —
+        // certification compares against tdd through A and B — so the
+        // fp32 stream forms it in fp32 from a float copy of u (known at
+        // the top of the step), keeping the double product and its two
+        // conversions off the scan -> ballot chain.
+        AT t;
+        if constexpr (F32) t = __fmul_rn(u32, T);
+        else t = static_cast<AT>(tdd);
+        // certification thresholds (T, u only): |t_ref - t| <= Mt
+        const double Thi = Td * (1.0 + 0x1.0p-16) + abs_q;
+        const double Mt = (e_rel + 4.0 * ulp_at) * (u * Thi) + abs_q; // + rounding of t to AT
+        const double A = tdd + Mt + 2.0 * abs_q; // need Pj * (1 - e) > A
+        const double B = tdd - Mt - 2.0 * abs_q; // need Pprev + e * Pj < B
+        bool ok = (T > AT(0)) && (Td < 1e300);
+        int next = -1;
+        if (ok) {
+            AT base = AT(0), my = AT(0);
+            int rs = -1;
 #pragma unroll
             for (int r = 0; r < MAXR; ++r) {
-                incl[r] = AT(0);
-                rtot[r] = AT(0);
-                if (r < p.R) {
-                    const int cbase = r * 32 * C + lane * C;
-                    const int w0 = cbase >> 5, sh = cbase & 31;
-                    uint32_t win[NWIN];
-#pragma unroll
-                    for (int i = 0; i < NWIN; ++i)
-                        win[i] = __funnelshift_r(tabu[w0 + i], tabu[w0 + i + 1], sh);
-                    const VT* rv = reinterpret_cast<const VT*>(rowsrc + r * kLP * C) + lane;
-                    WT gs[NG];
-#pragma unroll
-                    for (int g = 0; g < NG; ++g) {
-                        WT x[GE];
-#pragma unroll
-                        for (int tt = 0; tt < GV; ++tt) {
-                            const int tv = g * GV + tt;
-                            VT v;
-                            if (tv < NV) {
-                                v = rv[tv * kLP];
-                            } else {
-                                if constexpr (F32) v = make_float4(0.f, 0.f, 0.f, 0.f);
-                                else v = make_double2(0.0, 0.0);
-                            }
-                            if constexpr (F32) {
-                                x[tt * 4 + 0] = v.x; x[tt * 4 + 1] = v.y;
-                                x[tt * 4 + 2] = v.z; x[tt * 4 + 3] = v.w;
-                            } else {
-                                x[tt * 2 + 0] = v.x; x[tt * 2 + 1] = v.y;
-                            }
-                        }
-#pragma unroll
-                        for (int e = 0; e < GE; ++e) {
-                            const int ee = g * GE + e;
-                            if (ee < C && ((win[ee >> 5] >> (ee & 31)) & 1u)) x[e] = WT(0);
-                        }
-                        if constexpr (F32) gs[g] = tree_sum_packed<GE>(x);
-                        else gs[g] = tree_sum<WT, GE>(x);
-                        if constexpr (MAXR > 1) gsum[(r * NG + g) * 32 + lane] = gs[g];
+                if (r < p.R && rs < 0) {
+                    if (base + rtot[r] > t) {
+                        rs = r;
+                        my = incl[r];
+                    } else {
+                        base += rtot[r];
                     }
-                    if constexpr (MAXR == 1) { // lane-local inclusive group prefixes
-                        gsr[0] = gs[0];
+                }
+            }
+            int J = -1;        // candidate city (global index), valid in lane Q
+            bool cert = false; // its certification
+            if constexpr (kGroupWalk) {
+                // Group walk (MAXR == 1, fp32): every lane locates the
+                // crossing GROUP of its own chunk from its group prefixes
+                // (no extra shared reads); lane L's group G and exclusive
+                // base are broadcast, and lanes 0..3 each take one 4-city
+                // quad of that group: quad prefixes by three parallel
+                // shuffles, the first crossing city by one ballot.
+                const AT exo = __shfl_up_sync(kFull, incl[0], 1);
+                const AT excl_own = lane == 0 ? AT(0) : exo;
+                const unsigned lb = __ballot_sync(kFull, incl[0] > t);
+                // crossing group of the own chunk: the number of group
+                // prefixes <= t - excl_own (a wrong pick in a rounding tie
+                // only fails certification); its exclusive base.
+                const AT tl = t - excl_own;
+                int Gown = 0;
+                AT gb = AT(0);
 #pragma unroll
-                        for (int g = 1; g < NG; ++g) gsr[g] = gsr[g - 1] + gs[g];
+                for (int g = 0; g < NG; ++g) {
+                    const bool below = gsr[g] <= tl;
+                    Gown += below ? 1 : 0;
+                    gb = below ? gsr[g] : gb;
+                }
+                const AT bG = excl_own + gb;
+                if (lb) {
+                    const int L = __ffs(lb) - 1;
+                    const int G = __shfl_sync(kFull, Gown, L);
+                    const AT baseG = __shfl_sync(kFull, bG, L);
+                    if (G < NG) {
+                        const int k = lane & 3;
+                        const int tv = G * GV + k;
+                        const int c0 = L * C + tv * 4; // first city of the quad
+                        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                        uint32_t bits4 = 0xFu;
+                        if (tv < NV) {
+                            v = reinterpret_cast<const float4*>(buf)[tv * kLP + L];
+                            bits4 = __funnelshift_r(tabu[c0 >> 5], tabu[(c0 >> 5) + 1], c0 & 31);
+                        }
+                        AT x0 = (bits4 & 1u) ? AT(0) : v.x;
+                        AT x1 = (bits4 & 2u) ? AT(0) : v.y;
+                        AT x2 = (bits4 & 4u) ? AT(0) : v.z;
+                        AT x3 = (bits4 & 8u) ? AT(0) : v.w;
+                        const AT a1 = x0 + x1;
+                        const AT a2 = a1 + x2;
+                        const AT a3 = a2 + x3;
+                        const AT s1 = __shfl_up_sync(kFull, a3, 1, 4);
+                        const AT s2 = __shfl_up_sync(kFull, a3, 2, 4);
+                        const AT s3 = __shfl_up_sync(kFull, a3, 3, 4);
+                        const AT ex = (k >= 1 ? s1 : AT(0)) + ((k >= 2 ? s2 : AT(0)) + (k >= 3 ? s3 : AT(0)));
+                        const AT kb = baseG + ex;
+                        const AT p0 = kb + x0, p1 = kb + a1, p2 = kb + a2, p3 = kb + a3;
+                        int E = -1;
+                        AT Pj32 = AT(0), Pp32 = AT(0);
+                        // first q with x_q > 0 and P_q > t (descending so the lowest wins)
+                        if (x3 > AT(0) && p3 > t) { E = 3; Pj32 = p3; Pp32 = p2; }
+                        if (x2 > AT(0) && p2 > t) { E = 2; Pj32 = p2; Pp32 = p1; }
+                        if (x1 > AT(0) && p1 > t) { E = 1; Pj32 = p1; Pp32 = p0; }
+                        if (x0 > AT(0) && p0 > t) { E = 0; Pj32 = p0; Pp32 = kb; }
+                        const unsigned qb = __ballot_sync(kFull, lane < 4 && E >= 0);
+                        const bool mine = qb != 0u && lane == __ffs(qb) - 1;
+                        // The certification in fp32 with directed rounding
+                        // (implies the fp64 form): Pj*lo_f >= rd(Pj*lo32) >
+                        // A32 >= A and Pprev + e*Pj <= ru(Pprev + ru(e32*Pj))
+                        // < B32 <= B, with lo32 <= lo_f, e32 >= e_rel.
+                        const float A32 = __double2float_ru(A);
+                        const float B32 = __double2float_rd(B);
+                        const int Jc = c0 + E;
+                        J = mine ? Jc : -1;
+                        cert = mine && (__fmul_rd(Pj32, lo32) > A32) &&
+                               (__fadd_ru(Pp32, __fmul_ru(e32, Pj32)) < B32) && Jc < n;
                     }
-                    AT d = static_cast<AT>(tree_sum<WT, NG>(gs));
-                    TICK(0);
+                }
+            } else {
+                // crossing lane L of round rs, then a cooperative walk over L's
+                // chunk: lane k takes quad k (4 consecutive cities), quad sums are
+                // scanned across the warp, and the lane holding the crossing quad
+                // walks its 4 cities.
+                const unsigned lb = __ballot_sync(kFull, rs >= 0 && base + my > t);
+                int Q = -1;
+                if (lb) {
+                    const int L = __ffs(lb) - 1;
+                    const AT myprev = __shfl_sync(kFull, my, L == 0 ? 0 : L - 1);
+                    const AT exclL = base + (L == 0 ? AT(0) : myprev);
+                    constexpr int NQT = C / 4; // quads per chunk
+                    const int cbaseL = rs * 32 * C + L * C;
+                    // all lanes load (lanes >= NQT re-read quad 0 and drop it)
+                    const int ql = lane < NQT ? lane : 0;
+                    AT xv[4];
                     if constexpr (F32) {
-                        d = warp_inclusive_scan(d);
+                        const float4* qp = reinterpret_cast<const float4*>(
+                            rowsrc + rs * kLP * C + (ql * kLP + L) * 4);
+                        const float4 v = *qp;
+                        xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
+                    } else {
+                        const double2 v0 = *reinterpret_cast<const double2*>(
+                            buf + rs * kLP * C + ((2 * ql) * kLP + L) * 2);
+                        const double2 v1 = *reinterpret_cast<const double2*>(
+                            buf + rs * kLP * C + ((2 * ql + 1) * kLP + L) * 2);
+                        xv[0] = v0.x; xv[1] = v0.y; xv[2] = v1.x; xv[3] = v1.y;
+                    }
+                    {
+                        const int c0 = cbaseL + 4 * ql;
+                        uint32_t bits4 =
+                            __funnelshift_r(tabu[c0 >> 5], tabu[(c0 >> 5) + 1], c0 & 31);
+                        if (lane >= NQT) bits4 = 0xFu;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if ((bits4 >> q) & 1u) xv[q] = AT(0);
+                    }
+                    const AT qs = (xv[0] + xv[1]) + (xv[2] + xv[3]);
+                    AT qi = qs;
+                    if constexpr (F32) {
+                        qi = warp_inclusive_scan(qi);
                     } else {
 #pragma unroll
                         for (int off = 1; off < 32; off <<= 1) {
-                            const AT y = __shfl_up_sync(kFull, d, off);
-                            if (lane >= off) d += y;
+                            const AT y = __shfl_up_sync(kFull, qi, off);
+                            if (lane >= off) qi += y;
                         }
                     }
-                    incl[r] = d;
-                    rtot[r] = __shfl_sync(kFull, d, 31);
-                    T += rtot[r];
-                    TICK(1);
+                    const AT qe = __shfl_up_sync(kFull, qi, 1);
+                    const unsigned qb = __ballot_sync(kFull, lane < NQT && exclL + qi > t);
+                    Q = __ffs(qb) - 1;
+                    // every lane walks its own quad; only lane Q's result is kept
+                    AT ea = exclL + (lane == 0 ? AT(0) : qe);
+                    AT Pj32 = AT(0), Pp32 = AT(0);
+                    int E = -1;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const AT na = ea + xv[q];
+                        const bool hit = (E < 0) && (xv[q] > AT(0)) && (na > t);
+                        Pj32 = hit ? na : Pj32;
+                        Pp32 = hit ? ea : Pp32;
+                        E = hit ? q : E;
+                        ea = na;
+                    }
+                    const double Pj = static_cast<double>(Pj32);
+                    const double Pprev = static_cast<double>(Pp32);
+                    const int Jc = cbaseL + 4 * lane + E;
+                    const bool mine = (lane == Q) && (E >= 0);
+                    J = mine ? Jc : -1;
+                    cert = mine && (Pj * lo_f > A) && (Pprev + e_rel * Pj < B) && Jc < n;
                 }
             }
-            const double Td = static_cast<double>(T);
-            const double tdd = u * Td;
-            // Candidate threshold in AT.  Only the candidate search uses it —
-            // certification compares against tdd through A and B — so the
-            // fp32 stream forms it in fp32 from a float copy of u (known at
-            // the top of the step), keeping the double product and its two
-            // conversions off the scan -> ballot chain.
-            AT t;
-            if constexpr (F32) t = __fmul_rn(u32, T);
-            else t = static_cast<AT>(tdd);
-            // certification thresholds (T, u only): |t_ref - t| <= Mt
-            const double Thi = Td * (1.0 + 0x1.0p-16) + abs_q;
-            const double Mt = (e_rel + 4.0 * ulp_at) * (u * Thi) + abs_q; // + rounding of t to AT
-            const double A = tdd + Mt + 2.0 * abs_q; // need Pj * (1 - e) > A
-            const double B = tdd - Mt - 2.0 * abs_q; // need Pprev + e * Pj < B
-            bool ok = (T > AT(0)) && (Td < 1e300);
-            int next = -1;
+            TICK(2);
+            // speculative refill, issued by the certifying lane itself: every
+            // read of buf in this step has returned (its value fed the ballots)
+            if (cert && step + 1 < n) {
+                mbar_expect_tx(bar, row_bytes);
+                tma_row(buf, wbase + static_cast<size_t>(J) * p.PW, row_bytes, bar);
+            }
+            const unsigned cb = __ballot_sync(kFull, cert);
+            ok = cb != 0u;
             if (ok) {
-                AT base = AT(0), my = AT(0);
-                int rs = -1;
-#pragma unroll
-                for (int r = 0; r < MAXR; ++r) {
-                    if (r < p.R && rs < 0) {
-                        if (base + rtot[r] > t) {
-                            rs = r;
-                            my = incl[r];
-                        } else {
-                            base += rtot[r];
-                        }
-                    }
-                }
-                int J = -1;        // candidate city (global index), valid in lane Q
-                bool cert = false; // its certification
-                if constexpr (kGroupWalk) {
-                    // Group walk (MAXR == 1, fp32): every lane locates the
-                    // crossing GROUP of its own chunk from its group prefixes
-                    // (no extra shared reads); lane L's group G and exclusive
-                    // base are broadcast, and lanes 0..3 each take one 4-city
-                    // quad of that group: quad prefixes by three parallel
-                    // shuffles, the first crossing city by one ballot.
-                    const AT exo = __shfl_up_sync(kFull, incl[0], 1);
-                    const AT excl_own = lane == 0 ? AT(0) : exo;
-                    const unsigned lb = __ballot_sync(kFull, incl[0] > t);
-                    // crossing group of the own chunk: the number of group
-                    // prefixes <= t - excl_own (a wrong pick in a rounding tie
-                    // only fails certification); its exclusive base.
-                    const AT tl = t - excl_own;
-                    int Gown = 0;
-                    AT gb = AT(0);
-#pragma unroll
-                    for (int g = 0; g < NG; ++g) {
-                        const bool below = gsr[g] <= tl;
-                        Gown += below ? 1 : 0;
-                        gb = below ? gsr[g] : gb;
-                    }
-                    const AT bG = excl_own + gb;
-                    if (lb) {
-                        const int L = __ffs(lb) - 1;
-                        const int G = __shfl_sync(kFull, Gown, L);
-                        const AT baseG = __shfl_sync(kFull, bG, L);
-                        if (G < NG) {
-                            const int k = lane & 3;
-                            const int tv = G * GV + k;
-                            const int c0 = L * C + tv * 4; // first city of the quad
-                            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                            uint32_t bits4 = 0xFu;
-                            if (tv < NV) {
-                                v = reinterpret_cast<const float4*>(buf)[tv * kLP + L];
-                                bits4 = __funnelshift_r(tabu[c0 >> 5], tabu[(c0 >> 5) + 1], c0 & 31);
-                            }
-                            AT x0 = (bits4 & 1u) ? AT(0) : v.x;
-                            AT x1 = (bits4 & 2u) ? AT(0) : v.y;
-                            AT x2 = (bits4 & 4u) ? AT(0) : v.z;
-                            AT x3 = (bits4 & 8u) ? AT(0) : v.w;
-                            const AT a1 = x0 + x1;
-                            const AT a2 = a1 + x2;
-                            const AT a3 = a2 + x3;
-                            const AT s1 = __shfl_up_sync(kFull, a3, 1, 4);
-                            const AT s2 = __shfl_up_sync(kFull, a3, 2, 4);
-                            const AT s3 = __shfl_up_sync(kFull, a3, 3, 4);
-                            const AT ex = (k >= 1 ? s1 : AT(0)) + ((k >= 2 ? s2 : AT(0)) + (k >= 3 ? s3 : AT(0)));
-                            const AT kb = baseG + ex;
-                            const AT p0 = kb + x0, p1 = kb + a1, p2 = kb + a2, p3 = kb + a3;
-                            int E = -1;
-                            AT Pj32 = AT(0), Pp32 = AT(0);
-                            // first q with x_q > 0 and P_q > t (descending so the lowest wins)
-                            if (x3 > AT(0) && p3 > t) { E = 3; Pj32 = p3; Pp32 = p2; }
-                            if (x2 > AT(0) && p2 > t) { E = 2; Pj32 = p2; Pp32 = p1; }
-                            if (x1 > AT(0) && p1 > t) { E = 1; Pj32 = p1; Pp32 = p0; }
-                            if (x0 > AT(0) && p0 > t) { E = 0; Pj32 = p0; Pp32 = kb; }
-                            const unsigned qb = __ballot_sync(kFull, lane < 4 && E >= 0);
-                            const bool mine = qb != 0u && lane == __ffs(qb) - 1;
-                            // The certification in fp32 with directed rounding
-                            // (implies the fp64 form): Pj*lo_f >= rd(Pj*lo32) >
-                            // A32 >= A and Pprev + e*Pj <= ru(Pprev + ru(e32*Pj))
-                            // < B32 <= B, with lo32 <= lo_f, e32 >= e_rel.
-                            const float A32 = __double2float_ru(A);
-                            const float B32 = __double2float_rd(B);
-                            const int Jc = c0 + E;
-                            J = mine ? Jc : -1;
-                            cert = mine && (__fmul_rd(Pj32, lo32) > A32) &&
-                                   (__fadd_ru(Pp32, __fmul_ru(e32, Pj32)) < B32) && Jc < n;
-                        }
-                    }
-                } else {
-                    // crossing lane L of round rs, then a cooperative walk over L's
-                    // chunk: lane k takes quad k (4 consecutive cities), quad sums are
-                    // scanned across the warp, and the lane holding the crossing quad
-                    // walks its 4 cities.
-                    const unsigned lb = __ballot_sync(kFull, rs >= 0 && base + my > t);
-                    int Q = -1;
-                    if (lb) {
-                        const int L = __ffs(lb) - 1;
-                        const AT myprev = __shfl_sync(kFull, my, L == 0 ? 0 : L - 1);
-                        const AT exclL = base + (L == 0 ? AT(0) : myprev);
-                        constexpr int NQT = C / 4; // quads per chunk
-                        const int cbaseL = rs * 32 * C + L * C;
-                        // all lanes load (lanes >= NQT re-read quad 0 and drop it)
-                        const int ql = lane < NQT ? lane : 0;
-                        AT xv[4];
-                        if constexpr (F32) {
-                            const float4* qp = reinterpret_cast<const float4*>(
-                                rowsrc + rs * kLP * C + (ql * kLP + L) * 4);
-                            const float4 v = *qp;
-                            xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
-                        } else {
-                            const double2 v0 = *reinterpret_cast<const double2*>(
-                                buf + rs * kLP * C + ((2 * ql) * kLP + L) * 2);
-                            const double2 v1 = *reinterpret_cast<const double2*>(
-                                buf + rs * kLP * C + ((2 * ql + 1) * kLP + L) * 2);
-                            xv[0] = v0.x; xv[1] = v0.y; xv[2] = v1.x; xv[3] = v1.y;
-                        }
-                        {
-                            const int c0 = cbaseL + 4 * ql;
-                            uint32_t bits4 =
-                                __funnelshift_r(tabu[c0 >> 5], tabu[(c0 >> 5) + 1], c0 & 31);
-                            if (lane >= NQT) bits4 = 0xFu;
-    #pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                if ((bits4 >> q) & 1u) xv[q] = AT(0);
-                        }
-                        const AT qs = (xv[0] + xv[1]) + (xv[2] + xv[3]);
-                        AT qi = qs;
-                        if constexpr (F32) {
-                            qi = warp_inclusive_scan(qi);
-                        } else {
-    #pragma unroll
-                            for (int off = 1; off < 32; off <<= 1) {
-                                const AT y = __shfl_up_sync(kFull, qi, off);
-                                if (lane >= off) qi += y;
-                            }
-                        }
-                        const AT qe = __shfl_up_sync(kFull, qi, 1);
-                        const unsigned qb = __ballot_sync(kFull, lane < NQT && exclL + qi > t);
-                        Q = __ffs(qb) - 1;
-                        // every lane walks its own quad; only lane Q's result is kept
-                        AT ea = exclL + (lane == 0 ? AT(0) : qe);
-                        AT Pj32 = AT(0), Pp32 = AT(0);
-                        int E = -1;
-    #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const AT na = ea + xv[q];
-                            const bool hit = (E < 0) && (xv[q] > AT(0)) && (na > t);
-                            Pj32 = hit ? na : Pj32;
-                            Pp32 = hit ? ea : Pp32;
-                            E = hit ? q : E;
-                            ea = na;
-                        }
-                        const double Pj = static_cast<double>(Pj32);
-                        const double Pprev = static_cast<double>(Pp32);
-                        const int Jc = cbaseL + 4 * lane + E;
-                        const bool mine = (lane == Q) && (E >= 0);
-                        J = mine ? Jc : -1;
-                        cert = mine && (Pj * lo_f > A) && (Pprev + e_rel * Pj < B) && Jc < n;
-                    }
-                }
-                TICK(2);
-                // speculative refill, issued by the certifying lane itself: every
-                // read of buf in this step has returned (its value fed the ballots)
-                if (cert && step + 1 < n) {
-                    mbar_expect_tx(bar, row_bytes);
-                    tma_row(buf, wbase + static_cast<size_t>(J) * p.PW, row_bytes, bar);
-                }
-                const unsigned cb = __ballot_sync(kFull, cert);
-                ok = cb != 0u;
-                if (ok) {
-                    next = __shfl_sync(kFull, J, __ffs(cb) - 1);
-                    prefetched = step + 1 < n;
-                }
+                next = __shfl_sync(kFull, J, __ffs(cb) - 1);
+                prefetched = step + 1 < n;
             }
-            TICK(3);
-            if (!ok) { // middle tier: fp64 sums over the fp32 row still in smem
-                const int j2 = certify_fp64<WT, NV, MAXR>(buf, tabu, n, p.R, u, lane);
-                if (j2 >= 0) {
-                    ok = true;
-                    next = j2;
-                    ++fb2;
-                }
-            }
-            if (!ok) {
-                if (prefetched) { // never set when !ok, kept for safety
-                    mbar_wait(bar, phase);
-                    phase ^= 1u;
-                    prefetched = false;
-                }
-                next = exact_walk(p.w64 + static_cast<size_t>(cur) * p.P64, tabu, n,
-                                  p.tabu_words, u, lane, chunk_start,
-                                  reinterpret_cast<double*>(buf), row_bytes & ~255u, bar, phase);
-                phase ^= static_cast<uint32_t>(exact_walk_pieces(n, row_bytes & ~255u) & 1);
-                ++fb;
-            }
-            TICK(4);
-            // Every read of the shared tabu in this step has been consumed by a
-            // ballot/shuffle, so lane 0 updates it without a barrier; the
-            // __syncwarp before the next step's mbarrier wait orders it before
-            // any later read.
-            if (lane == 0) {
-                tabu[next >> 5] |= 1u << (next & 31);
-                tour[step] = next;
-            }
-            if constexpr (STREAM) hs.put(p, kl, step, next, lane);
-            cur = next;
-            TICK(5);
         }
+        TICK(3);
+        if (!ok) { // middle tier: fp64 sums over the fp32 row still in smem
+            const int j2 = certify_fp64<WT, NV, MAXR>(buf, tabu, n, p.R, u, lane);
+            if (j2 >= 0) {
+                ok = true;
+                next = j2;
+                ++fb2;
+            }
+        }
+        if (!ok) {
+            if (prefetched) { // never set when !ok, kept for safety
+                mbar_wait(bar, phase);
+                phase ^= 1u;
+                prefetched = false;
+            }
+            next = exact_walk(p.w64 + static_cast<size_t>(cur) * p.P64, tabu, n,
+                              p.tabu_words, u, lane, chunk_start,
+                              reinterpret_cast<double*>(buf), row_bytes & ~255u, bar, phase);
+            phase ^= static_cast<uint32_t>(exact_walk_pieces(n, row_bytes & ~255u) & 1);
+            ++fb;
+        }
+        TICK(4);
+        // Every read of the shared tabu in this step has been consumed by a
+        // ballot/shuffle, so lane 0 updates it without a barrier; the
+        // __syncwarp before the next step's mbarrier wait orders it before
+        // any later read.
+        if (lane == 0) {
+            tabu[next >> 5] |= 1u << (next & 31);
+            tour[step] = next;
+        }
+        if constexpr (STREAM) hs.put(p, kl, step, next, lane);
+        cur = next;
+        TICK(5);
+    }
 #if ACO_TIMING
-        if (lane == 0 && p.timing)
-            for (int i = 0; i < 7; ++i) atomicAdd(p.timing + i, ph[i]);
+    if (lane == 0 && p.timing)
+        for (int i = 0; i < 7; ++i) atomicAdd(p.timing + i, ph[i]);
 #endif
 #undef TICK
-        if (lane == 0) {
-            tour[n] = start;
-            if (fb) atomicAdd(p.fallbacks, fb);
-            if (fb2) atomicAdd(p.tier2, fb2);
+    a.cur = cur;
+    a.prefetched = prefetched;
+    a.hs = hs;
+}
+
+template <typename WT, int NV, int MAXR, bool STREAM = false>
+__global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(ConstructParams p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    uint32_t* tabu = reinterpret_cast<uint32_t*>(smem_raw + 128 + static_cast<size_t>(p.PW) * sizeof(WT));
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) mbar_init(bar, 1);
+    __syncwarp();
+    uint32_t phase = 0;
+    unsigned long long fb = 0, fb2 = 0;
+    for (int kl = blockIdx.x; kl < p.mloc; kl += gridDim.x) {
+        RouletteAnt a;
+        roulette_begin(p, a, kl, tabu, lane, STREAM);
+        roulette_steps<WT, NV, MAXR, STREAM>(p, a, 1, p.n, smem_raw, phase, fb, fb2);
+        roulette_end(p, a, lane, STREAM);
+    }
+    if (lane == 0) {
+        if (fb) atomicAdd(p.fallbacks, fb);
+        if (fb2) atomicAdd(p.tier2, fb2);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Relay variant of the fp32 single-round roulette.  With q = floor(m / SMs)
+// warps on every SM and E = m - q*SMs leftover ants, the plain launch puts a
+// (q+1)-th warp on E SMs; that warp shares an SM sub-partition (5 warps on
+// one scheduler at q = 16) and holds the whole kernel back.  Here the grid is
+// q*SMs warps, warp w builds ant w, and each leftover ant x is built in K
+// segments by warps x, x+E, .., x+(K-1)E: warp x+iE runs its own ant up to
+// the segment's first step, waits for segment i-1 to be handed over (building
+// its own ant meanwhile), builds the segment, hands the tabu set and current
+// city on, and finishes its own ant.  Every warp's work is the same steps of
+// the same ants with the same draws, so tours are identical to the plain
+// kernel's.  All runs of steps go through ONE inlined call site of the step
+// loop (a small state machine picks the ant and the step range), so the hot
+// loop compiles like the plain kernel's; only the run boundaries touch the
+// two ants' state in local memory.
+__device__ __forceinline__ void roulette_drain(RouletteAnt& a, uint64_t* bar, uint32_t& phase) {
+    if (a.prefetched) { // a speculative row for this ant is in flight
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        a.prefetched = false;
+    }
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* q) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(q) : "memory");
+    return v;
+}
+
+template <int NV, bool STREAM>
+__global__ void __launch_bounds__(32, 16) k_construct_roulette_relay(ConstructParams p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+    uint32_t* tabu_own = reinterpret_cast<uint32_t*>(smem_raw + 128 + static_cast<size_t>(p.PW) * sizeof(float));
+    // after chunk_start (single-round rows have no gsum area)
+    uint32_t* tabu_rel = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(tabu_own + p.tabu_words) +
+                                                     ((p.n + 31) >> 5));
+    const int lane = threadIdx.x & 31;
+    const int n = p.n;
+    if (lane == 0) mbar_init(bar, 1);
+    __syncwarp();
+    uint32_t phase = 0;
+    unsigned long long fb = 0, fb2 = 0;
+    const int kl = blockIdx.x; // grid == relay_W: one own ant per warp
+    const int rx = kl % p.relay_E, ri = kl / p.relay_E;
+    const bool has_seg = ri < p.relay_K;
+    const int seg_begin = has_seg ? relay_bound(ri, p.relay_K, n) : n;
+    const int seg_end = has_seg ? relay_bound(ri + 1, p.relay_K, n) : n;
+    const unsigned long long stamp = (p.relay_epoch << 20) | static_cast<unsigned>(ri);
+    RouletteAnt ants[2]; // [0] own ant, [1] the relayed ant during the segment
+    roulette_begin(p, ants[0], kl, tabu_own, lane, STREAM);
+    int s = 1;                     // the own ant's next step
+    int stage = has_seg ? 0 : 3;   // 0 own before the segment, 1 segment, 2 own after, 3 own only
+    for (;;) {
+        int which = 0, s0 = s, s1 = n;
+        if (stage == 0) {
+            if (s < seg_begin) {
+                s1 = seg_begin;
+            } else {
+                bool ready = ri == 0;
+                if (!ready) {
+                    unsigned long long f = 0;
+                    if (lane == 0) f = ld_acquire_u64(p.relay_flag + rx);
+                    ready = __shfl_sync(kFull, f, 0) == stamp;
+                }
+                if (!ready) { // build the own ant one step further meanwhile
+                    if (s >= n) {
+                        __nanosleep(256);
+                        continue;
+                    }
+                    s1 = s + 1;
+                } else {
+                    if (ri > 0) (void)ld_acquire_u64(p.relay_flag + rx); // order every lane's reads
+                    roulette_drain(ants[0], bar, phase);
+                    RouletteAnt& r = ants[1];
+                    if (ri == 0) {
+                        roulette_begin(p, r, p.relay_W + rx, tabu_rel, lane, STREAM);
+                    } else {
+                        r.kl = p.relay_W + rx;
+                        r.kg = static_cast<uint32_t>(p.ant_begin + r.kl);
+                        r.tour = p.tours + static_cast<size_t>(r.kl) * (n + 1);
+                        r.tabu = tabu_rel;
+                        r.prefetched = false;
+                        r.hs = TourStream{0};
+                        const uint32_t* src = p.relay_tabu + static_cast<size_t>(rx) * p.tabu_words;
+                        for (int wd = lane; wd < p.tabu_words; wd += 32) tabu_rel[wd] = __ldcg(src + wd);
+                        r.cur = __ldcg(p.relay_cur + rx);
+                        __syncwarp();
+                    }
+                    which = 1;
+                    s0 = seg_begin;
+                    s1 = seg_end;
+                    stage = 1;
+                }
+            }
+        } else if (stage == 1) { // segment built: hand it over (or close the tour)
+            RouletteAnt& r = ants[1];
+            roulette_drain(r, bar, phase);
+            __syncwarp();
+            if (seg_end == n) {
+                roulette_end(p, r, lane, STREAM);
+            } else {
+                uint32_t* dst = p.relay_tabu + static_cast<size_t>(rx) * p.tabu_words;
+                for (int wd = lane; wd < p.tabu_words; wd += 32) __stcg(dst + wd, tabu_rel[wd]);
+                if (lane == 0) __stcg(p.relay_cur + rx, r.cur);
+                __threadfence();
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.relay_flag + rx),
+                                 "l"(stamp + 1)
+                                 : "memory");
+            }
+            stage = 2;
+            if (s >= n) break;
+        } else if (stage == 2) {
+            break;
+        } else {
+            stage = 2;
         }
-        if constexpr (STREAM) {
-            hs.put(p, kl, n, start, lane);
-            hs.flush(p, kl, n, lane);
-        }
-        __syncwarp();
+        roulette_steps<float, NV, 1, STREAM>(p, ants[which], s0, s1, smem_raw, phase, fb, fb2);
+        if (which == 0) s = s1;
+    }
+    roulette_end(p, ants[0], lane, STREAM);
+    if (lane == 0) {
+        if (fb) atomicAdd(p.fallbacks, fb);
+        if (fb2) atomicAdd(p.tier2, fb2);
     }
 }
 
