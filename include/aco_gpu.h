@@ -233,6 +233,17 @@ void* aco_gpu_stream(aco_gpu_ctx* ctx);
  *   the sharded device path on one GPU; statistics are per shard.) */
 aco_status aco_gpu_exchange_buffers(aco_gpu_ctx* ctx, void** succ, void** pred, void** inv,
                                     void** delta, int32_t* shard_stride, int32_t* P64);
+/* Row-sharded gather deposit in EXTERNAL-EXCHANGE mode (world > 1, gather
+ * deposit, rows of <= ~4000 doubles): after the caller delivered, from every
+ * rank g, g's succ/pred rows [rank*B, rank*B + B) (B = ceil(n / world)) and
+ * the 1/C_k blocks, folds this rank's row block into delta rows
+ * [rank*B, rank*B + B) (delta row pitch P64); the caller then all-gathers the
+ * delta row blocks and calls aco_gpu_update, which applies them to every row
+ * (pheromone.hpp:213-228, bit-identical to the replicated fold).  With an
+ * NCCL id the engine does this itself inside aco_gpu_update.  Without a
+ * preceding aco_gpu_fold, aco_gpu_update folds all rows (replicated).
+ * ACO_E_CONFIG_ERROR when the context does not row-shard; *row_blk = B. */
+aco_status aco_gpu_fold(aco_gpu_ctx* ctx, int32_t* row_blk);
 /* Human-readable name + launch shape of the last construction kernel
  * (e.g. "k_construct_roulette<float,19,1> grid=2392 per_sm=17 ..."); copies at
  * most len-1 bytes + NUL into buf, returns the full length.  Empty before the

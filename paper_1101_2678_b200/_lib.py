@@ -66,7 +66,7 @@ EXPORTS = [
     "aco_gpu_construct", "aco_gpu_update", "aco_gpu_iterate", "aco_gpu_get_pheromone",
     "aco_gpu_get_choice", "aco_gpu_get_choice32", "aco_gpu_get_topk", "aco_gpu_get_tours", "aco_gpu_get_best",
     "aco_gpu_get_info", "aco_gpu_stream", "aco_gpu_exchange_buffers", "aco_gpu_launch_count", "aco_gpu_describe", "aco_gpu_nccl_unique_id",
-    "aco_gpu_philox_uniform", "aco_gpu_validate_tours", "aco_gpu_libm_pow",
+    "aco_gpu_philox_uniform", "aco_gpu_validate_tours", "aco_gpu_libm_pow", "aco_gpu_fold",
 ]
 
 _p = C.c_void_p
@@ -103,6 +103,7 @@ def _load() -> C.CDLL:
     L.aco_gpu_compute_choice_info.argtypes = [_p]
     L.aco_gpu_construct.argtypes = [_p, C.POINTER(aco_gpu_iter_record)]
     L.aco_gpu_update.argtypes = [_p, C.POINTER(aco_gpu_iter_record)]
+    L.aco_gpu_fold.argtypes = [_p, C.POINTER(C.c_int32)]
     L.aco_gpu_iterate.argtypes = [_p, C.POINTER(aco_gpu_iter_record), _p, _p]
     L.aco_gpu_libm_pow.argtypes = [_i32, _i32, _p, _p, _p]
     L.aco_gpu_validate_tours.argtypes = [_p, _p, _p, _i32]

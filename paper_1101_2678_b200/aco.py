@@ -466,6 +466,14 @@ class Engine:
         _check(lib.aco_gpu_construct(self._h, C.byref(r)), self._h)
         return self._record(r)
 
+    def fold(self) -> int:
+        """Row-sharded gather deposit, external-exchange mode (aco_gpu_fold):
+        folds this rank's row block into the delta rows; returns the block
+        size B (rows [rank*B, rank*B+B))."""
+        b = C.c_int32()
+        _check(lib.aco_gpu_fold(self._h, C.byref(b)), self._h)
+        return b.value
+
     def update(self) -> IterationRecord:
         r = _lib.aco_gpu_iter_record()
         _check(lib.aco_gpu_update(self._h, C.byref(r)), self._h)

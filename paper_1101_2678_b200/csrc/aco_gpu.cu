@@ -43,6 +43,8 @@ struct NcclApi {
                               cudaStream_t) = nullptr;
     ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -64,6 +66,8 @@ NcclApi& nccl() {
             api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
             api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
             api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
+            api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+            api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
             api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
             api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
             api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
@@ -213,6 +217,11 @@ struct aco_gpu_ctx {
     uint32_t* d_relay_tabu = nullptr;           // [num_sms][tabu_words]
     unsigned long long relay_epoch = 0;
     double* d_dnn = nullptr;            // nn + accumulate: compact n x nn deposit slots
+    // gather deposit with world > 1: row-sharded fold (rank r folds rows
+    // [r*row_blk, (r+1)*row_blk) into delta rows, which are all-gathered)
+    bool row_shard = false;
+    int row_blk = 0;
+    bool folded = false; // external mode: aco_gpu_fold ran this iteration
     ncclComm_t comm = nullptr;
     bool external = false; // world > 1 without an NCCL id: the caller exchanges
     bool sharded = false;  // the sharded protocol (world > 1, or a 1-rank NCCL communicator)
@@ -363,6 +372,10 @@ void launch_topk(aco_gpu_ctx* c) {
     check_launch(c, "k_row_topk");
 }
 
+// host-side launch modes of the row-sharded gather (c->row_shard): fold this
+// rank's row block into delta rows / apply the (all-gathered) delta rows
+constexpr int MODE_FOLD_OWN = 100, MODE_APPLY = 101;
+
 void launch_rows(aco_gpu_ctx* c, int mode) {
     RowParams rp{};
     rp.tau = c->d_tau;
@@ -397,6 +410,28 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
     rp.powtab = c->d_powtab;
     rp.delta_fix = c->d_delta_fix;
     rp.stats = c->d_stats;
+    rp.row_begin = 0;
+    rp.row_end = c->n;
+    if (mode == MODE_FOLD_OWN || mode == MODE_APPLY) { // row-sharded gather (c->row_shard)
+        if (mode == MODE_FOLD_OWN) {
+            rp.row_begin = std::min(c->n, c->rank * c->row_blk);
+            rp.row_end = std::min(c->n, rp.row_begin + c->row_blk);
+            const size_t wsmem0 = static_cast<size_t>(c->P64) * sizeof(double) + 64 * sizeof(double);
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_gather_warp<false>, 32, wsmem0));
+            const int grid = std::max(1, std::min(std::max(1, rp.row_end - rp.row_begin), per_sm * c->num_sms));
+            k_rows_gather_warp<false><<<grid, 32, wsmem0, c->stream>>>(rp);
+            check_launch(c, "k_rows_gather_warp");
+            return;
+        }
+        const size_t dsmem = (rp.choice32 || rp.choice_perm64) ? static_cast<size_t>(c->P64) * sizeof(double) : 0;
+        if (dsmem > 48 * 1024)
+            CK(cudaFuncSetAttribute(k_rows<MODE_DELTA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
+        k_rows<MODE_DELTA><<<std::min(c->n, c->num_sms * 8), 256, dsmem, c->stream>>>(rp);
+        check_launch(c, "k_rows");
+        launch_topk(c);
+        return;
+    }
     const size_t smem = static_cast<size_t>(c->P64) * sizeof(double);
     const size_t wsmem = smem + 64 * sizeof(double);
     if (mode == MODE_GATHER && wsmem <= 32 * 1024) { // one warp per row
@@ -968,7 +1003,41 @@ void do_update(aco_gpu_ctx* c) {
     }
     if (c->sharded && !c->external) {
         auto& api = nccl();
-        if (gather_mode(c)) {
+        if (gather_mode(c) && c->row_shard) {
+            // rank q needs, from every rank g, g's succ/pred rows of q's row
+            // block: [g][q*B .. q*B+rows_q) of the [world][n][S] tables
+            const size_t blk = static_cast<size_t>(c->n) * c->S;
+            const int B = c->row_blk;
+            auto rows_of = [&](int q) { return std::max(0, std::min(c->n, (q + 1) * B) - q * B); };
+            NK(api.GroupStart());
+            for (int q = 0; q < c->world; ++q) {
+                if (q == c->rank) continue;
+                const size_t out_off = c->rank * blk + static_cast<size_t>(q) * B * c->S;
+                const size_t out_cnt = static_cast<size_t>(rows_of(q)) * c->S;
+                const size_t in_off = q * blk + static_cast<size_t>(c->rank) * B * c->S;
+                const size_t in_cnt = static_cast<size_t>(rows_of(c->rank)) * c->S;
+                if (out_cnt) {
+                    NK(api.Send(c->d_succ + out_off, out_cnt, ncclInt32, q, c->comm, c->stream));
+                    NK(api.Send(c->d_pred + out_off, out_cnt, ncclInt32, q, c->comm, c->stream));
+                }
+                if (in_cnt) {
+                    NK(api.Recv(c->d_succ + in_off, in_cnt, ncclInt32, q, c->comm, c->stream));
+                    NK(api.Recv(c->d_pred + in_off, in_cnt, ncclInt32, q, c->comm, c->stream));
+                }
+            }
+            NK(api.AllGather(c->d_inv + static_cast<size_t>(c->rank) * c->S, c->d_inv, c->S,
+                             ncclFloat64, c->comm, c->stream));
+            NK(api.GroupEnd());
+            CK(cudaEventRecord(c->ev[3], c->stream));
+            launch_rows(c, MODE_FOLD_OWN);
+            const size_t dblk = static_cast<size_t>(B) * c->P64;
+            NK(api.AllGather(c->d_delta + c->rank * dblk, c->d_delta, dblk, ncclFloat64, c->comm,
+                             c->stream));
+            launch_rows(c, MODE_APPLY);
+            CK(cudaEventRecord(c->ev[4], c->stream));
+            CK(cudaEventRecord(c->ev[5], c->stream));
+            return;
+        } else if (gather_mode(c)) {
             const size_t blk = static_cast<size_t>(c->n) * c->S;
             NK(api.GroupStart());
             NK(api.AllGather(c->d_succ + c->rank * blk, c->d_succ, blk, ncclInt32, c->comm, c->stream));
@@ -990,7 +1059,11 @@ void do_update(aco_gpu_ctx* c) {
         }
     }
     CK(cudaEventRecord(c->ev[3], c->stream));
-    if (gather_mode(c)) {
+    if (gather_mode(c) && c->external && c->folded) { // aco_gpu_fold ran: apply the gathered delta rows
+        c->folded = false;
+        launch_rows(c, MODE_APPLY);
+        CK(cudaEventRecord(c->ev[4], c->stream));
+    } else if (gather_mode(c)) {
         launch_rows(c, MODE_GATHER);
         CK(cudaEventRecord(c->ev[4], c->stream));
     } else if (c->sharded) {
@@ -1361,10 +1434,20 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
             CK(cudaMalloc(&c->d_delta_fix, cells * sizeof(unsigned long long)));
             CK(cudaMemset(c->d_delta_fix, 0, cells * sizeof(unsigned long long)));
         }
+        // Gather deposit over several ranks: each folds only its block of
+        // ceil(n/world) rows (the succ/pred rows of that block arrive from every
+        // rank by send/recv instead of an all-gather of the whole tables) and
+        // the delta rows are all-gathered (ACO_ROW_SHARD=0: replicated fold).
+        const char* rsh = std::getenv("ACO_ROW_SHARD");
+        c->row_shard = c->sharded && c->world > 1 && warp_gather && !(gsplit && gsplit[0] == '0') &&
+                       !(rsh && rsh[0] == '0');
+        c->row_blk = c->row_shard ? (n + c->world - 1) / c->world : n;
         if ((c->sharded && c->cfg.deposit == ACO_DEP_ACCUMULATE && !c->fixed) ||
             (warp_gather && !(gsplit && gsplit[0] == '0'))) {
-            CK(cudaMalloc(&c->d_delta, cells * sizeof(double)));
-            CK(cudaMemset(c->d_delta, 0, cells * sizeof(double)));
+            // row-sharded: world row blocks of row_blk rows (the last one padded)
+            const size_t dcells = std::max(cells, static_cast<size_t>(c->world) * c->row_blk * c->P64);
+            CK(cudaMalloc(&c->d_delta, dcells * sizeof(double)));
+            CK(cudaMemset(c->d_delta, 0, dcells * sizeof(double)));
             // fp32 wire only on request (aco_gpu_params::wire): the default
             // all-reduces the fp64 delta, so tours do not depend on G
             if (c->sharded && !c->external && c->cfg.deposit == ACO_DEP_ACCUMULATE &&
@@ -1532,6 +1615,21 @@ aco_status aco_gpu_construct(aco_gpu_ctx* c, aco_gpu_iter_record* rec) {
         r->fallbacks = fb0 + fb1;
         r->certified_fp64 = c->h_stats[10];
         r->best_so_far = c->best_so_far;
+    });
+}
+
+aco_status aco_gpu_fold(aco_gpu_ctx* c, int32_t* row_blk) {
+    if (c && !(c->external && c->row_shard)) {
+        c->err = "aco_gpu_fold: the context does not row-shard its gather deposit "
+                 "(needs external-exchange mode, world > 1, a gather deposit and rows of <= ~4000 doubles)";
+        return ACO_E_CONFIG_ERROR;
+    }
+    return guard_ctx(c, [&] {
+        CK(cudaSetDevice(c->device));
+        launch_rows(c, MODE_FOLD_OWN);
+        CK(cudaStreamSynchronize(c->stream));
+        c->folded = true;
+        if (row_blk) *row_blk = c->row_blk;
     });
 }
 

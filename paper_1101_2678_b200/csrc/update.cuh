@@ -490,6 +490,7 @@ struct RowParams {
     const LibmPowTables* powtab; // host libm's pow tables (alpha not in {0, 1})
     unsigned long long* delta_fix; // MODE_DELTA_FIX: n x P64 fixed-point sums
     const long long* stats;        // MODE_DELTA_FIX: stats[7] = the scale exponent s
+    int row_begin, row_end;        // k_rows_gather_warp: the rows this launch folds
 };
 
 // Write one row of the permuted streamed layout (stream_pos) from the natural
@@ -747,7 +748,7 @@ __global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
     const int lane = threadIdx.x & 31;
     const int n = p.n;
     constexpr int AHEAD = ACO_GATHER_AHEAD;
-    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    for (int i = p.row_begin + blockIdx.x; i < p.row_end; i += gridDim.x) {
         double* trow = p.tau + static_cast<size_t>(i) * p.P64;
         for (int j = lane; j < n; j += 32) rowbuf[j] = 0.0;
         __syncwarp();

@@ -91,6 +91,58 @@ def test_virtual_shards_match_single_context(deposit, G, m):
         e.close()
 
 
+@pytest.mark.parametrize("G,n,m", [(2, 300, 300), (3, 301, 301), (8, 300, 2400)])
+def test_row_sharded_gather_fold_bit_exact(G, n, m):
+    """The row-sharded gather deposit: shard r folds only
+    rows [r*B, r*B+B) of the ordered deposit into delta rows (aco_gpu_fold),
+    the delta row blocks are all-gathered (here by the test), and every shard
+    applies them (aco_gpu_update) — tau and choice bit-identical with the
+    single-context colony on every shard (pheromone.hpp:213-228)."""
+    import torch
+
+    from paper_1101_2678_b200 import aco
+
+    prob, single, shards = _engines(aco, n, m, 1, G)
+    bufs = [e.exchange_buffers() for e in shards]
+    S, P64 = bufs[0]["S"], bufs[0]["P64"]
+    B = -(-n // G)
+    for it in range(3):
+        single.run_iteration()
+        for e in shards:
+            e.construct()
+        torch.cuda.synchronize()
+        # every shard's succ/pred rows of shard q's block go to shard q
+        for name in ("succ", "pred"):
+            views = [torch.as_tensor(DevArray(b[name], (G, n, S), "<i4"), device="cuda") for b in bufs]
+            for g in range(G):
+                for q in range(G):
+                    if q != g:
+                        views[q][g, q * B:min(n, (q + 1) * B)].copy_(views[g][g, q * B:min(n, (q + 1) * B)])
+        views = [torch.as_tensor(DevArray(b["inv"], (G * S,), "<f8"), device="cuda") for b in bufs]
+        for g in range(G):
+            for q in range(G):
+                if q != g:
+                    views[q][g * S:(g + 1) * S].copy_(views[g][g * S:(g + 1) * S])
+        torch.cuda.synchronize()
+        assert all(e.fold() == B for e in shards)
+        deltas = [torch.as_tensor(DevArray(b["delta"], (G * B, P64), "<f8"), device="cuda") for b in bufs]
+        for g in range(G):
+            for q in range(G):
+                if q != g:
+                    deltas[q][g * B:(g + 1) * B].copy_(deltas[g][g * B:(g + 1) * B])
+        torch.cuda.synchronize()
+        for e in shards:
+            e.update()
+        tau_ref, ch_ref = single.pheromone(), single.choice()
+        for e in shards:
+            assert np.array_equal(e.pheromone(), tau_ref), f"tau differs at iteration {it}"
+            assert np.array_equal(e.choice(), ch_ref)
+        got = np.concatenate([e.ants()[0] for e in shards])
+        assert np.array_equal(got, single.ants()[0])
+    for e in shards + [single]:
+        e.close()
+
+
 @pytest.mark.parametrize("deposit,wire", [(1, 0), (0, 0), (0, 1)])
 def test_nccl_exchange_path_one_rank(deposit, wire):
     """The NCCL exchange path (all-gather of succ/pred/1/C_k, or all-reduce of

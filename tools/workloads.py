@@ -54,11 +54,11 @@ def l2_and_hbm_peaks(device=0):
             else "live 2 GiB read (libaco_probe.so)"}
 
 
-def time_engine(aco, torch, prob, n, m, selection, deposit, G, iters, warmup, nn=30):
+def time_engine(aco, torch, prob, n, m, selection, deposit, G, iters, warmup, nn=30, wire=0):
     cfg = aco.RunConfig(params=aco.Parameters(m=m, seed=1, nn=nn),
                         selection=aco.SelectionStrategy(aco.Selection(selection)),
                         deposit=aco.DepositStrategy(aco.Deposit(deposit)),
-                        world=G, rank=0)
+                        world=G, rank=0, wire=aco.Wire(wire))
     eng = aco.Engine(prob, cfg)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     sp = torch.cuda.ExternalStream(eng.stream_handle(), device="cuda")
@@ -128,16 +128,25 @@ def rooflines(res, n, m_total, selection, deposit, nn, peaks):
     }
 
 
-def exchange_model(n, m_total, G, deposit):
+def exchange_model(n, m_total, G, deposit, wire_kind=0, selection=0, nn=30, records=0):
     """Bytes each GPU sends per iteration over NVLink and a labelled time model
-    (ring all-reduce / all-gather at 700 GB/s bus bandwidth; not measured)."""
+    (ring all-reduce / all-gather at 700 GB/s bus bandwidth; not measured).
+    wire_kind: 0 fp64 (default), 1 fp32, 2 fixed64 (int64 sums; nn selection:
+    compact n x nn slots + the non-list edge records)."""
     if G == 1:
         return None
     P = (n + 31) // 32 * 32
-    if deposit == 0:
-        size = n * P * 4  # fp32 wire (k_delta_pack), DESIGN §5
+    if deposit == 0 and wire_kind == 2 and selection == 1:
+        slots = n * nn * 8
+        rec = G * records * 16  # every rank's records, all-gathered
+        wire = 2 * (G - 1) / G * slots + (G - 1) / G * rec
+        what = (f"ncclAllReduce(slots, {n}x{nn} u64) + ncclAllGather(records, "
+                f"~{records} x 16 B per rank)")
+    elif deposit == 0:
+        esz = 4 if wire_kind == 1 else 8
+        size = n * P * esz
         wire = 2 * (G - 1) / G * size
-        what = f"ncclAllReduce(delta, {n}x{P} f32, sum) after k_delta_pack"
+        what = f"ncclAllReduce(delta, {n}x{P} {['f64', 'f32', 'u64'][wire_kind]}, sum)"
     else:
         S = -(-m_total // G)
         size = G * (2 * n * S * 4 + S * 8)
@@ -148,6 +157,15 @@ def exchange_model(n, m_total, G, deposit):
             "model": "bytes_per_gpu / 700 GB/s NVLink-5 bus bandwidth (not measured: 1-GPU box)"}
 
 
+def _records(res):
+    """nn + fixed64: non-list edges per shard ~ argmax fallbacks + one closing
+    edge per ant (from the engine's describe())."""
+    import re
+
+    m = re.search(r"argmax_fallbacks=(\d+)", res.get("kernel", ""))
+    return (int(m.group(1)) if m else 0) + res["m_local"]
+
+
 WORKLOADS = [
     # name, n, m (0 = n), selection, deposits, G list, iterations, cpu iterations
     ("d198", 198, 0, 0, (0, 1), (1,), 10, 10),
@@ -155,7 +173,11 @@ WORKLOADS = [
     ("pr2392", 2392, 0, 0, (0, 1), (1, 2, 4, 8), 10, 2),
     ("pr2392x8ants", 2392, 8 * 2392, 0, (0, 1), (1, 2, 4, 8), 5, 1),
     ("synth10k_nn30", 10000, 0, 1, (0,), (1, 8), 3, 1),
+    # config 5 on the exact fixed-point wire: the sharded exchange is the
+    # compact nn slots + records instead of the n^2 delta
+    ("synth10k_nn30_fixed64", 10000, 0, 1, (0,), (1, 8), 3, 0),
 ]
+WIRE = {"synth10k_nn30_fixed64": 2}
 
 
 def main():
@@ -180,19 +202,22 @@ def main():
             for G in Gs:
                 it = 2 if a.quick else iters
                 t0 = time.time()
-                res = time_engine(aco, torch, prob, n, m, sel, dep, G, it, 2)
+                wk = WIRE.get(name, 0)
+                res = time_engine(aco, torch, prob, n, m, sel, dep, G, it, 2, wire=wk)
                 res["G"] = G
                 res["wall_s"] = round(time.time() - t0, 1)
                 entry = {"workload": name, "n": n, "m": m_total, "G": G,
                          "selection": aco.selection_name(aco.Selection(sel)),
                          "deposit": aco.deposit_name(aco.Deposit(dep)), **res,
                          "roofline": rooflines(res, n, m_total, sel, dep, 30, peaks),
-                         "exchange": exchange_model(n, m_total, G, dep)}
+                         "wire": ["fp64", "fp32", "fixed64"][wk],
+                         "exchange": exchange_model(n, m_total, G, dep, wk, sel, 30,
+                                                    records=_records(res))}
                 if G > 1:
                     entry["ants_per_s_job"] = round(m_total / (res["ms_per_iter"] * 1e-3), 1)
                 print(json.dumps(entry), flush=True)
                 report["workloads"].append(entry)
-        if not (a.quick or a.no_cpu):
+        if not (a.quick or a.no_cpu) and cpu_iters:
             # reference CPU: accumulate always; the O(n^4) gather family only at d198
             for dep in deps:
                 if dep == 1 and n > 198:
