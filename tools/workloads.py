@@ -24,7 +24,9 @@ Rooflines:
       red.f64 deposit runs in the construction phase; shard emulation runs
       the fp64 external-exchange kernel — the NCCL path's k_delta_pack +
       k_rows<DELTA32> are timed separately by tools/pack_cost.py);
-  update (gather):         (8+8+4+8+S)*n*P + 16*m*n + 8*m, over HBM peak;
+  update (gather):         (8+8+4+8+S)*n*P + 16*m*n + 8*m, over HBM peak
+      (G > 1: the row-sharded fold of n/G rows + the apply of all rows,
+      timed around aco_gpu_fold + aco_gpu_update);
   S = 4 for the roulette's fp32 stream, 0 for nn; nn adds the top-K rebuild's
       8*n*P re-read of the choice rows.
 """
@@ -59,14 +61,49 @@ def time_engine(aco, torch, prob, n, m, selection, deposit, G, iters, warmup, nn
                         selection=aco.SelectionStrategy(aco.Selection(selection)),
                         deposit=aco.DepositStrategy(aco.Deposit(deposit)),
                         world=G, rank=0, wire=aco.Wire(wire))
+    if wire == 2 and G > 1:
+        # the fixed-point wire has no external-exchange mode: one GPU's share
+        # is emulated by a one-GPU colony of ceil(m/G) ants (the same kernels
+        # on the same number of ants; its own records only)
+        cfg.world = 1
+        cfg.params.m = -(-(m or n) // G)
     eng = aco.Engine(prob, cfg)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     sp = torch.cuda.ExternalStream(eng.stream_handle(), device="cuda")
     recs = []
+    rowshard = G > 1 and deposit != 0  # row-sharded gather: construct, fold, update
+    if rowshard:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from test_gpu_sharded import DevArray
+
+        xb = eng.exchange_buffers()
+        S = xb["S"]
+        tabs = [torch.as_tensor(DevArray(xb[k], (G, n, S), "<i4"), device="cuda") for k in ("succ", "pred")]
+        inv = torch.as_tensor(DevArray(xb["inv"], (G, S), "<f8"), device="cuda")
     for i in range(warmup + iters):
         with torch.cuda.stream(sp):
             flush.fill_(i & 0xFF)
-        r = eng.run_iteration()
+        if not rowshard:
+            r = eng.run_iteration()
+        else:
+            # rank 0's shard; the other ranks' succ/pred/1/C_k blocks stand in
+            # as copies of rank 0's (same duplicate statistics), so the fold
+            # of rank 0's n/G rows and the apply run on realistic data
+            r = eng.construct()
+            torch.cuda.synchronize()
+            for t in tabs + [inv]:
+                for g in range(1, G):
+                    t[g].copy_(t[0])
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(sp):
+                a.record(sp)
+            eng.fold()
+            eng.update()
+            with torch.cuda.stream(sp):
+                b.record(sp)
+            b.synchronize()
+            r.update_ms = a.elapsed_time(b)  # fold + apply, incl. two host calls
         if i >= warmup:
             recs.append(r)
     torch.cuda.synchronize()
@@ -116,6 +153,9 @@ def rooflines(res, n, m_total, selection, deposit, nn, peaks):
         b_u = (8 + 8 + 8 + 8 + 4 + 8 + s32) * n * P + topk
     elif deposit == 0:                         # evaporate + red.f64 + k_rows<CHOICE>
         b_u = 16 * n * P + 2 * m_total * n * 8 + 4 * m_total * (n + 1) + (8 + 4 + 8 + s32) * n * P + topk
+    elif res.get("G", 1) > 1:                  # row-sharded: fold n/G rows, apply all rows
+        B = -(-n // res["G"])
+        b_u = 8 * m_total * B + 8 * B * P + (8 + 8 + 8 + 4 + 8 + s32) * n * P + topk
     else:                                      # k_rows gather: tau r/w, dist, choice + succ/pred
         b_u = (8 + 8 + 4 + 8 + s32) * n * P + 16 * m_total * n + 8 * m_total + topk
     c_gbs = b_c / (res["construct_kernel_ms"] * 1e-3) / 1e9
@@ -147,11 +187,12 @@ def exchange_model(n, m_total, G, deposit, wire_kind=0, selection=0, nn=30, reco
         size = n * P * esz
         wire = 2 * (G - 1) / G * size
         what = f"ncclAllReduce(delta, {n}x{P} {['f64', 'f32', 'u64'][wire_kind]}, sum)"
-    else:
+    else:  # row-sharded gather
         S = -(-m_total // G)
-        size = G * (2 * n * S * 4 + S * 8)
-        wire = (G - 1) / G * size
-        what = "ncclAllGather(succ, pred int32 [G][n][S]; 1/C_k f64)"
+        B = -(-n // G)
+        wire = (G - 1) * (2 * B * S * 4 + S * 8 + B * P * 8)
+        what = ("ncclSend/Recv(succ, pred row blocks) + ncclAllGather(1/C_k) + "
+                "ncclAllGather(delta row blocks)")
     return {"collective": what, "bytes_per_gpu": int(wire),
             "modelled_ms": round(wire / 700e9 * 1e3, 4),
             "model": "bytes_per_gpu / 700 GB/s NVLink-5 bus bandwidth (not measured: 1-GPU box)"}
