@@ -638,17 +638,29 @@ void launch_construct(aco_gpu_ctx* c) {
         fn<<<grid, 32, smem, c->stream>>>(p);
         check_launch(c, "k_construct_roulette");
     } else if (c->cfg.selection == ACO_SEL_NN) {
+        // Early request of the crossing candidate's list (before its
+        // certification, k_construct_nn<true>, 64 registers) pays when the
+        // launch is latency-bound — few ants per SM: 10k with 1250 ants 8.06
+        // -> 7.56 ms, pr1002 0.678 -> 0.649 ms — and costs at full occupancy
+        // (10k, 10000 ants: 27.5 -> 30.6 ms; tools/lib_ab.py).
+        // ACO_NN_SPEC=0/1 forces the choice.
+        static const int spec_env = [] {
+            const char* e = std::getenv("ACO_NN_SPEC");
+            return e ? (e[0] == '1' ? 1 : 0) : -1;
+        }();
+        const bool spec = spec_env >= 0 ? spec_env == 1 : c->mloc <= 12 * c->num_sms;
+        auto nnfn = spec ? k_construct_nn<true> : k_construct_nn<false>;
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_construct_nn, 32, smem1));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nnfn, 32, smem1));
         const int grid = std::max(1, std::min(c->mloc, per_sm * c->num_sms));
         c->construct_grid = grid;
         c->construct_desc = "k_construct_nn grid=" + std::to_string(grid) +
-                            " per_sm=" + std::to_string(per_sm);
+                            " per_sm=" + std::to_string(per_sm) + (spec ? " spec" : "");
         if (fused_tail_enabled()) {
             p.len_out = c->d_len;
             c->fused_tail = true;
         }
-        k_construct_nn<<<grid, 32, smem1, c->stream>>>(p);
+        nnfn<<<grid, 32, smem1, c->stream>>>(p);
         check_launch(c, "k_construct_nn");
     } else {
         const size_t smem4 = smem1 * 4 + 4 * 1024 * sizeof(int);

@@ -1199,7 +1199,10 @@ __global__ void __launch_bounds__(32) k_construct_roulette_exact(ConstructParams
 #ifndef ACO_NN_MINB
 #define ACO_NN_MINB 16 // resident warps per SM the register budget must allow
 #endif
-__global__ void __launch_bounds__(32, ACO_NN_MINB) k_construct_nn(ConstructParams p) {
+// SPEC: the crossing candidate's list is requested before its certification
+// (for latency-bound launches; that variant is held to 64 registers)
+template <bool SPEC>
+__global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(ConstructParams p) {
     extern __shared__ uint32_t smem_tabu[];
     uint32_t* tabu = smem_tabu;
     const int lane = threadIdx.x & 31;
@@ -1232,6 +1235,11 @@ __global__ void __launch_bounds__(32, ACO_NN_MINB) k_construct_nn(ConstructParam
         const bool fast32 = nn <= 32 && p.choice_nn32 != nullptr;
         int jpre = -1;
         float wpre = 0.f;
+        // SPEC: the crossing candidate's list is requested before its
+        // certification
+        int jg = -1;
+        int jspec = -1;
+        float wspec = 0.f;
         if (fast32 && lane < nn) {
             jpre = p.nn_lists[static_cast<size_t>(start) * nn + lane];
             wpre = p.choice_nn32[static_cast<size_t>(start) * nn + lane];
@@ -1284,6 +1292,13 @@ __global__ void __launch_bounds__(32, ACO_NN_MINB) k_construct_nn(ConstructParam
                         const float PJ = __shfl_sync(kFull, P, J);
                         const float EJ = __shfl_sync(kFull, E, J);
                         const int Jc = __shfl_sync(kFull, j, J);
+                        if (SPEC && lane < nn && step + 1 < n) {
+                            // the candidate's list, requested before its
+                            // certification (which almost always passes)
+                            jg = Jc;
+                            jspec = p.nn_lists[static_cast<size_t>(Jc) * nn + lane];
+                            wspec = p.choice_nn32[static_cast<size_t>(Jc) * nn + lane];
+                        }
                         // thresholds in fp32, every operation rounded
                         // outward: A32 >= u*T + Mt + 2*abs, B32 <= u*T - Mt -
                         // 2*abs, Mt >= (e + 4*2^-24) * u * (T(1+2^-16) + abs)
@@ -1502,10 +1517,16 @@ __global__ void __launch_bounds__(32, ACO_NN_MINB) k_construct_nn(ConstructParam
                 }
                 next = bj;
             }
-            if (fast32 && lane < nn && step + 1 < n) {
-                jpre = p.nn_lists[static_cast<size_t>(next) * nn + lane];
-                wpre = p.choice_nn32[static_cast<size_t>(next) * nn + lane];
+            if (fast32 && step + 1 < n) {
+                if (SPEC && next == jg) { // the speculated list is the one
+                    jpre = jspec;
+                    wpre = wspec;
+                } else if (lane < nn) {
+                    jpre = p.nn_lists[static_cast<size_t>(next) * nn + lane];
+                    wpre = p.choice_nn32[static_cast<size_t>(next) * nn + lane];
+                }
             }
+            jg = -1;
             if (lane == 0) {
                 tabu[next >> 5] |= 1u << (next & 31);
                 tour[step] = next;
