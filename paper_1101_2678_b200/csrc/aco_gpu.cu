@@ -602,8 +602,8 @@ void launch_construct(aco_gpu_ctx* c) {
             const int W = q * c->num_sms;
             int K = relay_k_override();
             if (K <= 0) K = static_cast<int>(std::lround(std::sqrt(static_cast<double>(c->n - 1))));
-            K = std::max(1, std::min({K, W / E, (c->n - 1) / 64}));
-            if (rper_sm >= q && K >= 1 && (c->n - 1) / K >= 64) {
+            K = std::max(1, std::min({K, W / E, (c->n - 1) / 33}));
+            if (rper_sm >= q && K >= 1 && (c->n - 1) / K >= 33) {
                 if (!c->d_relay_flag) {
                     CK(cudaMalloc(&c->d_relay_flag, c->num_sms * sizeof(unsigned long long)));
                     CK(cudaMemsetAsync(c->d_relay_flag, 0, c->num_sms * sizeof(unsigned long long), c->stream));

@@ -63,10 +63,14 @@ template <> struct VecOf<double> {
 // vectors has LA + 1 slots (one pad slot) so that reading one lane's chunk
 // across a warp spreads over several bank groups.  Round r holds cities
 // [r*LA*C, (r+1)*LA*C) in (LA+1)*C elements.
-constexpr int kLP = 33; // (LA + 1) for LA = 32
+#ifndef ACO_PAD_SLOT
+#define ACO_PAD_SLOT 1
+#endif
+constexpr int kPad = ACO_PAD_SLOT;
+constexpr int kLP = 32 + kPad; // (LA + pad) for LA = 32
 
 __host__ __device__ __forceinline__ int stream_pos(int c, int C, int V, int LA = 32) {
-    const int RC = LA * C, LP = LA + 1;
+    const int RC = LA * C, LP = LA + kPad;
     const int r = c / RC, rem = c - r * RC;
     const int l = rem / C, e = rem - l * C;
     const int t = e / V, q = e - t * V;
@@ -75,7 +79,7 @@ __host__ __device__ __forceinline__ int stream_pos(int c, int C, int V, int LA =
 
 // Inverse of stream_pos; returns INT_MAX for pad slots.
 __host__ __device__ __forceinline__ int stream_city(int p, int C, int V, int LA = 32) {
-    const int LP = LA + 1, RS = LP * C;
+    const int LP = LA + kPad, RS = LP * C;
     const int r = p / RS, rem = p - r * RS;
     const int t = rem / (LP * V), rem2 = rem - t * LP * V;
     const int l = rem2 / V, q = rem2 - l * V;
@@ -140,7 +144,8 @@ struct ConstructParams {
 
 // First step of relay segment i of K over steps 1..n-1 (segment K ends at n);
 // inner bounds are multiples of 32, so a segment's tour-stream chunks and
-// Philox batches never straddle a hand-over (the host keeps (n-1)/K >= 64).
+// Philox batches never straddle a hand-over (the host keeps (n-1)/K >= 33,
+// so the 32-aligned bounds stay strictly increasing).
 __host__ __device__ __forceinline__ int relay_bound(int i, int K, int n) {
     if (i <= 0) return 1;
     if (i >= K) return n;

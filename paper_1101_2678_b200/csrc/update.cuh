@@ -502,7 +502,7 @@ template <int V, typename OT>
 __device__ __forceinline__ void write_stream_row(OT* __restrict__ crow, const double* rowbuf, int n,
                                                  int PW, int C, int LA, int sc, int tid,
                                                  int nthreads) {
-    const int LP = LA + 1, NVL = C / V, RS = LP * NVL; // vector slots per round
+    const int LP = LA + kPad, NVL = C / V, RS = LP * NVL; // vector slots per round
     const int nslots = PW / V;
     for (int s = tid; s < nslots; s += nthreads) {
         const int r = s / RS, rem = s - r * RS;
