@@ -1037,9 +1037,10 @@ void do_update(aco_gpu_ctx* c) {
                     NK(api.Recv(c->d_pred + in_off, in_cnt, ncclInt32, q, c->comm, c->stream));
                 }
             }
+            NK(api.GroupEnd());
+            // (the 1/C_k all-gather in its own call, not grouped with p2p)
             NK(api.AllGather(c->d_inv + static_cast<size_t>(c->rank) * c->S, c->d_inv, c->S,
                              ncclFloat64, c->comm, c->stream));
-            NK(api.GroupEnd());
             CK(cudaEventRecord(c->ev[3], c->stream));
             launch_rows(c, MODE_FOLD_OWN);
             const size_t dblk = static_cast<size_t>(B) * c->P64;
@@ -1494,6 +1495,7 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         if (c->sharded && !c->external) {
             auto& api = nccl();
             if (!api.CommInitRank) throw Fail{ACO_E_NCCL, "libnccl.so.2 not found"};
+            if (!api.Send || !api.Recv) c->row_shard = false; // pre-p2p NCCL: replicated fold
             ncclUniqueId id;
             std::memcpy(&id, prm->nccl_id, sizeof(id));
             NK(api.CommInitRank(&c->comm, c->world, id, c->rank));
