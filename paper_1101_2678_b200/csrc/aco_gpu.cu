@@ -216,6 +216,14 @@ struct aco_gpu_ctx {
     int32_t* d_relay_cur = nullptr;             // [num_sms]
     uint32_t* d_relay_tabu = nullptr;           // [num_sms][tabu_words]
     unsigned long long relay_epoch = 0;
+    // resolved roulette launch shape, [0] plain / [1] streaming tours to host
+    struct RouletteLaunch {
+        bool valid = false, relay = false;
+        void (*fn)(acob200::ConstructParams) = nullptr;
+        size_t smem = 0;
+        int grid = 0, W = 0, E = 0, K = 0;
+        std::string desc;
+    } rlaunch[2];
     double* d_dnn = nullptr;            // nn + accumulate: compact n x nn deposit slots
     // gather deposit with world > 1: row-sharded fold (rank r folds rows
     // [r*row_blk, (r+1)*row_blk) into delta rows, which are all-gathered)
@@ -566,6 +574,12 @@ void launch_construct(aco_gpu_ctx* c) {
         check_launch(c, "k_construct_roulette_exact");
     } else if (c->cfg.selection == ACO_SEL_ROULETTE) {
         const bool st = c->host_tours != nullptr;
+        // the launch shape (kernel, shared memory, grid, relay split) is
+        // resolved once per context and tours-to-host mode: the occupancy
+        // queries and attribute calls stay off the per-iteration host path,
+        // where the GPU would idle waiting for the first launch
+        auto& L = c->rlaunch[st ? 1 : 0];
+        if (!L.valid) {
         ConstructFn fn = c->stream_kind == ACO_STREAM_FP64 ? pick_roulette<double>(c->NV, c->MAXR, st)
                                                            : pick_roulette<float>(c->NV, c->MAXR, st);
         const size_t wsz = c->stream_kind == ACO_STREAM_FP64 ? sizeof(double) : sizeof(float);
@@ -611,13 +625,10 @@ void launch_construct(aco_gpu_ctx* c) {
                     CK(cudaMalloc(&c->d_relay_tabu,
                                   static_cast<size_t>(c->num_sms) * c->tabu_words * sizeof(uint32_t)));
                 }
-                p.relay_W = W;
-                p.relay_E = E;
-                p.relay_K = K;
-                p.relay_epoch = ++c->relay_epoch;
-                p.relay_flag = c->d_relay_flag;
-                p.relay_cur = c->d_relay_cur;
-                p.relay_tabu = c->d_relay_tabu;
+                L.relay = true;
+                L.W = W;
+                L.E = E;
+                L.K = K;
                 fn = rfn;
                 smem = rsmem;
                 per_sm = rper_sm;
@@ -626,16 +637,31 @@ void launch_construct(aco_gpu_ctx* c) {
                              " K=" + std::to_string(K);
             }
         }
-        c->construct_grid = grid;
-        c->construct_desc = std::string("k_construct_roulette<") +
-                            (c->stream_kind == ACO_STREAM_FP64 ? "double," : "float,") +
-                            std::to_string(c->NV) + "," + std::to_string(c->MAXR) + "> grid=" +
-                            std::to_string(grid) + " per_sm=" + std::to_string(per_sm) +
-                            " smem=" + std::to_string(smem) + " row=" + std::to_string(c->PW) +
-                            (st ? " streams_tours_to_host" : "") + relay_desc;
+        L.fn = fn;
+        L.smem = smem;
+        L.grid = grid;
+        L.desc = std::string("k_construct_roulette<") +
+                 (c->stream_kind == ACO_STREAM_FP64 ? "double," : "float,") +
+                 std::to_string(c->NV) + "," + std::to_string(c->MAXR) + "> grid=" +
+                 std::to_string(grid) + " per_sm=" + std::to_string(per_sm) +
+                 " smem=" + std::to_string(smem) + " row=" + std::to_string(c->PW) +
+                 (st ? " streams_tours_to_host" : "") + relay_desc;
+        L.valid = true;
+        }
+        if (L.relay) {
+            p.relay_W = L.W;
+            p.relay_E = L.E;
+            p.relay_K = L.K;
+            p.relay_epoch = ++c->relay_epoch;
+            p.relay_flag = c->d_relay_flag;
+            p.relay_cur = c->d_relay_cur;
+            p.relay_tabu = c->d_relay_tabu;
+        }
+        c->construct_grid = L.grid;
+        c->construct_desc = L.desc;
         if (debug_enabled())
             std::fprintf(stderr, "construct: %s\n", c->construct_desc.c_str());
-        fn<<<grid, 32, smem, c->stream>>>(p);
+        L.fn<<<L.grid, 32, L.smem, c->stream>>>(p);
         check_launch(c, "k_construct_roulette");
     } else if (c->cfg.selection == ACO_SEL_NN) {
         // Early request of the crossing candidate's list (before its
