@@ -649,6 +649,14 @@ void launch_construct(aco_gpu_ctx* c) {
         L.valid = true;
         }
         if (L.relay) {
+            // fused tour tail only at high occupancy, where it overlaps other
+            // warps' steps (m = n = 2392: construct 3.853 -> 3.834 ms); with
+            // 4-8 warps per SM it lengthens the kernel more than the
+            // k_tour_length launch it saves (1196 ants: 2.820 -> 2.874 ms)
+            if (fused_tail_enabled() && L.W >= 12 * c->num_sms) {
+                p.len_out = c->d_len;
+                c->fused_tail = true;
+            }
             p.relay_W = L.W;
             p.relay_E = L.E;
             p.relay_K = L.K;

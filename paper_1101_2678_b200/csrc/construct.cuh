@@ -1110,6 +1110,7 @@ __global__ void __launch_bounds__(32, 16) k_construct_roulette_relay(ConstructPa
             __syncwarp();
             if (seg_end == n) {
                 roulette_end(p, r, lane, STREAM);
+                if (ACO_FUSED_TAIL_BUILD && p.len_out) tour_tail(p, r.tour, r.kl, lane);
             } else {
                 uint32_t* dst = p.relay_tabu + static_cast<size_t>(rx) * p.tabu_words;
                 for (int wd = lane; wd < p.tabu_words; wd += 32) __stcg(dst + wd, tabu_rel[wd]);
@@ -1132,6 +1133,9 @@ __global__ void __launch_bounds__(32, 16) k_construct_roulette_relay(ConstructPa
         if (which == 0) s = s1;
     }
     roulette_end(p, ants[0], lane, STREAM);
+    // fused tour tail (lengths, 1/C_k, succ/pred): the relay kernel has the
+    // register room the plain one lacks (128 vs 96)
+    if (ACO_FUSED_TAIL_BUILD && p.len_out) tour_tail(p, ants[0].tour, ants[0].kl, lane);
     if (lane == 0) {
         if (fb) atomicAdd(p.fallbacks, fb);
         if (fb2) atomicAdd(p.tier2, fb2);

@@ -26,6 +26,7 @@ with aco.Engine(prob, cfg) as e:
         h.update(e.ants()[0].tobytes())
     recs = recs[2:]
     print(json.dumps({"kernel_ms": round(statistics.median(r.construct_kernel_ms for r in recs), 4),
+                      "construct_ms": round(statistics.median(r.construct_ms for r in recs), 4),
                       "update_ms": round(statistics.median(r.update_ms for r in recs), 4),
                       "tours": h.hexdigest()[:12]}))
 """
