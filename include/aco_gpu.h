@@ -118,7 +118,9 @@ typedef struct {
      *  ACO_WIRE_MULTIMEM: FIXED64 whose deposit reds go straight into an NVLS
      *    multicast object (every GPU's delta at once, multimem.red.add.u64)
      *    with a flag barrier through the same object: no collective (needs
-     *    world > 1 on one NVSwitch node; world == 1 runs FIXED64).
+     *    world > 1 on one NVSwitch node; world == 1 runs FIXED64, and so does
+     *    a node where the multicast object cannot be created or its fabric
+     *    handle exported — every rank agrees, aco_gpu_describe reports it).
      * Every rank of a colony must pass the same value. */
     int32_t wire;
     /* Debug mode (TourBuffer::make pheromone.hpp:67-90 and

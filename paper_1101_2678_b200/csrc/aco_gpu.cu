@@ -203,6 +203,7 @@ struct aco_gpu_ctx {
     CUdeviceptr mc_uc = 0, mc_va = 0;
     size_t mc_size = 0;
     unsigned long long mc_epoch = 0;
+    bool mc_fallback = false; // MULTIMEM requested, multicast unavailable: FIXED64 all-reduce
     // nn + fixed-point accumulate: compact int64 slots + non-list edge records
     unsigned long long* d_dnn_fix = nullptr;   // n x nn
     DepositRecord* d_rec = nullptr;            // this rank's records (capacity mloc * n)
@@ -736,10 +737,31 @@ void nccl_barrier(aco_gpu_ctx* c) {
     cudaFree(d);
 }
 
-void setup_multicast(aco_gpu_ctx* c) {
+void teardown_multicast(aco_gpu_ctx* c);
+
+// every rank's verdict on a setup step (MIN over the ranks), so that all ranks
+// take the same branch and none is left waiting in a collective
+bool all_ranks_ok(aco_gpu_ctx* c, bool ok) {
+    int32_t* d = nullptr;
+    int32_t h = ok ? 1 : 0;
+    CK(cudaMalloc(&d, sizeof(int32_t)));
+    CK(cudaMemcpyAsync(d, &h, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+    NK(nccl().AllReduce(d, d, 1, ncclInt32, ncclMin, c->comm, c->stream));
+    CK(cudaMemcpyAsync(&h, d, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(d);
+    return h == 1;
+}
+
+// Returns false (every rank alike, nothing left allocated) when the node
+// cannot host the multicast object — no NVSwitch multicast, no fabric-handle
+// export (IMEX) — and the caller falls back to the FIXED64 all-reduce, which
+// gives the same integers.
+bool setup_multicast(aco_gpu_ctx* c) {
     DriverApi& d = driver();
-    if (!d.MulticastCreate || !d.MulticastBindMem || !d.MemImportFromShareableHandle)
-        throw Fail{ACO_E_UNSUPPORTED, "NVLS multicast exchange: driver entry points unavailable"};
+    const bool have = d.MulticastCreate && d.MulticastBindMem && d.MemImportFromShareableHandle &&
+                      d.MulticastAddDevice && d.MemCreate && d.MemMap && d.MulticastGetGranularity;
+    if (!all_ranks_ok(c, have)) return false;
     const CUmemAllocationHandleType ht = CU_MEM_HANDLE_TYPE_FABRIC;
     const size_t cells = static_cast<size_t>(c->n) * c->P64;
     const size_t want = cells * sizeof(unsigned long long) + 256; // delta + barrier flag
@@ -748,47 +770,63 @@ void setup_multicast(aco_gpu_ctx* c) {
     mp.handleTypes = ht;
     mp.size = want;
     size_t gran = 0;
-    mc_check(d.MulticastGetGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED),
-             "cuMulticastGetGranularity");
+    bool ok = d.MulticastGetGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED) == CUDA_SUCCESS &&
+              gran > 0;
+    if (!all_ranks_ok(c, ok)) return false;
     c->mc_size = (want + gran - 1) / gran * gran;
     mp.size = c->mc_size;
-    CUmemFabricHandle fh{};
+    // rank 0 creates and exports; the handle (and whether that worked) goes
+    // to every rank over the engine's communicator
+    struct {
+        CUmemFabricHandle fh;
+        int32_t ok;
+    } msg{};
     if (c->rank == 0) {
-        mc_check(d.MulticastCreate(&c->mc_handle, &mp), "cuMulticastCreate");
-        mc_check(d.MemExportToShareableHandle(&fh, c->mc_handle, ht, 0), "cuMemExportToShareableHandle");
+        ok = d.MulticastCreate(&c->mc_handle, &mp) == CUDA_SUCCESS;
+        if (ok) ok = d.MemExportToShareableHandle(&msg.fh, c->mc_handle, ht, 0) == CUDA_SUCCESS;
+        msg.ok = ok ? 1 : 0;
     }
     uint8_t* dh = nullptr;
-    CK(cudaMalloc(&dh, sizeof(fh)));
-    CK(cudaMemcpyAsync(dh, &fh, sizeof(fh), cudaMemcpyHostToDevice, c->stream));
-    NK(nccl().Broadcast(dh, dh, sizeof(fh), ncclUint8, 0, c->comm, c->stream));
-    CK(cudaMemcpyAsync(&fh, dh, sizeof(fh), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMalloc(&dh, sizeof(msg)));
+    CK(cudaMemcpyAsync(dh, &msg, sizeof(msg), cudaMemcpyHostToDevice, c->stream));
+    NK(nccl().Broadcast(dh, dh, sizeof(msg), ncclUint8, 0, c->comm, c->stream));
+    CK(cudaMemcpyAsync(&msg, dh, sizeof(msg), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     cudaFree(dh);
-    if (c->rank != 0)
-        mc_check(d.MemImportFromShareableHandle(&c->mc_handle, &fh, ht), "cuMemImportFromShareableHandle");
-    mc_check(d.MulticastAddDevice(c->mc_handle, static_cast<CUdevice>(c->device)), "cuMulticastAddDevice");
-    nccl_barrier(c); // every device joined before any memory is bound
+    ok = msg.ok == 1;
+    if (ok && c->rank != 0)
+        ok = d.MemImportFromShareableHandle(&c->mc_handle, &msg.fh, ht) == CUDA_SUCCESS;
+    if (ok) ok = d.MulticastAddDevice(c->mc_handle, static_cast<CUdevice>(c->device)) == CUDA_SUCCESS;
+    if (!all_ranks_ok(c, ok)) { // every device joined before any memory is bound
+        teardown_multicast(c);
+        return false;
+    }
     CUmemAllocationProp ap{};
     ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     ap.location.id = c->device;
     ap.requestedHandleTypes = ht;
-    mc_check(d.MemCreate(&c->mc_phys, c->mc_size, &ap, 0), "cuMemCreate");
-    mc_check(d.MulticastBindMem(c->mc_handle, 0, c->mc_phys, 0, c->mc_size, 0), "cuMulticastBindMem");
     CUmemAccessDesc acc{};
     acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     acc.location.id = c->device;
     acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    mc_check(d.MemAddressReserve(&c->mc_uc, c->mc_size, gran, 0, 0), "cuMemAddressReserve");
-    mc_check(d.MemMap(c->mc_uc, c->mc_size, 0, c->mc_phys, 0), "cuMemMap(unicast)");
-    mc_check(d.MemSetAccess(c->mc_uc, c->mc_size, &acc, 1), "cuMemSetAccess(unicast)");
-    mc_check(d.MemAddressReserve(&c->mc_va, c->mc_size, gran, 0, 0), "cuMemAddressReserve");
-    mc_check(d.MemMap(c->mc_va, c->mc_size, 0, c->mc_handle, 0), "cuMemMap(multicast)");
-    mc_check(d.MemSetAccess(c->mc_va, c->mc_size, &acc, 1), "cuMemSetAccess(multicast)");
+    ok = d.MemCreate(&c->mc_phys, c->mc_size, &ap, 0) == CUDA_SUCCESS;
+    if (ok) ok = d.MulticastBindMem(c->mc_handle, 0, c->mc_phys, 0, c->mc_size, 0) == CUDA_SUCCESS;
+    if (ok) ok = d.MemAddressReserve(&c->mc_uc, c->mc_size, gran, 0, 0) == CUDA_SUCCESS;
+    if (ok) ok = d.MemMap(c->mc_uc, c->mc_size, 0, c->mc_phys, 0) == CUDA_SUCCESS;
+    if (ok) ok = d.MemSetAccess(c->mc_uc, c->mc_size, &acc, 1) == CUDA_SUCCESS;
+    if (ok) ok = d.MemAddressReserve(&c->mc_va, c->mc_size, gran, 0, 0) == CUDA_SUCCESS;
+    if (ok) ok = d.MemMap(c->mc_va, c->mc_size, 0, c->mc_handle, 0) == CUDA_SUCCESS;
+    if (ok) ok = d.MemSetAccess(c->mc_va, c->mc_size, &acc, 1) == CUDA_SUCCESS;
+    if (!all_ranks_ok(c, ok)) {
+        teardown_multicast(c);
+        return false;
+    }
     CK(cudaMemsetAsync(reinterpret_cast<void*>(c->mc_uc), 0, c->mc_size, c->stream));
     nccl_barrier(c); // zeroed everywhere before the first red arrives
     c->d_delta_fix = reinterpret_cast<unsigned long long*>(c->mc_uc);
     c->multimem = true;
+    return true;
 }
 
 void teardown_multicast(aco_gpu_ctx* c) {
@@ -1533,7 +1571,13 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
             ncclUniqueId id;
             std::memcpy(&id, prm->nccl_id, sizeof(id));
             NK(api.CommInitRank(&c->comm, c->world, id, c->rank));
-            if (mc_wanted) setup_multicast(c);
+            if (mc_wanted && !setup_multicast(c)) {
+                // no multicast object on this node: the FIXED64 all-reduce of
+                // the same exact int64 sums (aco_gpu_describe says which ran)
+                CK(cudaMalloc(&c->d_delta_fix, cells * sizeof(unsigned long long)));
+                CK(cudaMemset(c->d_delta_fix, 0, cells * sizeof(unsigned long long)));
+                c->mc_fallback = true;
+            }
         }
 
         if (c->cfg.alpha != 0.0 && c->cfg.alpha != 1.0) {
@@ -1600,6 +1644,8 @@ int64_t aco_gpu_launch_count(const aco_gpu_ctx* c) { return c ? c->launches : 0;
 int32_t aco_gpu_describe(const aco_gpu_ctx* c, char* buf, int32_t len) {
     if (!c) return 0;
     std::string d = c->construct_desc;
+    if (c->multimem) d += " exchange=multimem";
+    else if (c->mc_fallback) d += " exchange=fixed64 (multicast unavailable)";
     if (c->cfg.selection == ACO_SEL_NN)
         d += " argmax_fallbacks=" + std::to_string(c->last_fb[1]) + " full_row_scans=" +
              std::to_string(c->last_fb[0]) + (c->d_topk ? " topk=" + std::to_string(kTopK) : " topk=off");

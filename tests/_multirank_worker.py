@@ -71,6 +71,7 @@ def main():
                 "exchange_ms": rec.exchange_ms,
             })
         dist.barrier()
+    report["describe"] = eng.describe()  # e.g. "exchange=multimem" or its fixed64 fallback
     eng.close()
     if rank == 0:
         single.close()
