@@ -1502,7 +1502,12 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         // nn + fixed: compact slots + records exchange; the dense int64 delta
         // stays local (no multicast needed — the exchange is already small)
         const bool nn_fixed = c->fixed && c->cfg.selection == ACO_SEL_NN;
-        const bool mc_wanted = c->fixed && prm->wire == ACO_WIRE_MULTIMEM && c->world > 1 && !nn_fixed;
+        // (ACO_MC_ONE_RANK=1: also attempt the multicast object on a one-rank
+        // communicator — a test hook for the agreement / fallback path, since
+        // cuMulticastCreate refuses a one-device object)
+        const char* mc1 = std::getenv("ACO_MC_ONE_RANK");
+        const bool mc_wanted = c->fixed && prm->wire == ACO_WIRE_MULTIMEM && !nn_fixed && c->sharded &&
+                               !c->external && (c->world > 1 || (mc1 && mc1[0] == '1'));
         if (nn_fixed) {
             const size_t ml2 = std::max(1, c->mloc);
             CK(cudaMalloc(&c->d_qpos, ml2 * n));

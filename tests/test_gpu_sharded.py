@@ -256,3 +256,34 @@ def test_fixed_point_deposit_within_tolerance_of_reference(oracle, selection):
             worst = max(worst, rel)
             tau = tau_ref
         assert worst <= 1e-12
+
+
+def test_multimem_setup_agrees_and_falls_back(monkeypatch):
+    """MULTIMEM (f2) where the NVLS multicast object cannot be created — here a
+    one-rank communicator, which cuMulticastCreate refuses — every rank agrees
+    (MIN all-reduce per setup step), nothing is left allocated, and the
+    engine runs the FIXED64 all-reduce of the same exact int64 sums: tau is
+    bit-identical with the fixed64 wire and describe() says which exchange
+    ran (pheromone.hpp:195-208)."""
+    from paper_1101_2678_b200 import aco
+
+    monkeypatch.setenv("ACO_MC_ONE_RANK", "1")
+    n = 300
+    prob = aco.build_problem(aco.synthetic_instance(n))
+
+    def eng(wire):
+        return aco.Engine(prob, aco.RunConfig(
+            params=aco.Parameters(m=0, seed=7),
+            selection=aco.SelectionStrategy(aco.Selection.roulette_full),
+            deposit=aco.DepositStrategy(aco.Deposit.accumulate),
+            nccl_id=aco.nccl_unique_id(), wire=aco.Wire(wire)))
+
+    a, b = eng(3), eng(2)
+    assert "multicast unavailable" in a.describe()
+    for _ in range(3):
+        a.run_iteration()
+        b.run_iteration()
+        assert np.array_equal(a.ants()[0], b.ants()[0])
+        assert np.array_equal(a.pheromone(), b.pheromone())
+    a.close()
+    b.close()
