@@ -40,6 +40,9 @@
 #ifndef ACO_LDG
 #define ACO_LDG 2 // 1: ld.global.nc.L1::no_allocate; 2: ld.global.nc (L1-allocating)
 #endif
+#ifndef ACO_SCAN_FMA
+#define ACO_SCAN_FMA 1 // warp scan levels as shfl + fma (see warp_inclusive_scan); 0: shfl + predicated add + select
+#endif
 #ifndef ACO_TIMING
 #define ACO_TIMING 0 // per-phase clock64() accounting into ConstructParams::timing
 #endif
@@ -395,8 +398,21 @@ __device__ __forceinline__ float scan_up_add(float v, int off) {
     return y;
 }
 __device__ __forceinline__ float warp_inclusive_scan(float v) {
+#if ACO_SCAN_FMA
+    // two dependent instructions per level instead of three: with m = 1 for
+    // lanes >= off (else 0), fma(y, m, v) is fl(v + y) or exactly v — the
+    // same values as scan_up_add for the finite non-negative sums scanned
+    // here (0 * y = +0 needs y finite)
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const float y = __shfl_up_sync(kFull, v, off);
+        v = __fmaf_rn(y, lane >= off ? 1.f : 0.f, v);
+    }
+#else
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) v = scan_up_add(v, off);
+#endif
     return v;
 }
 
