@@ -615,8 +615,12 @@ void launch_construct(aco_gpu_ctx* c) {
             int rper_sm = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rper_sm, rfn, 32, rsmem));
             const int W = q * c->num_sms;
+            // K ~ sqrt(n) segments of >= 64 steps (pr2392: K = 37; 20 and 49-74
+            // measured no better, profiles/relay_k_ab_r02.txt)
             int K = relay_k_override();
-            if (K <= 0) K = static_cast<int>(std::lround(std::sqrt(static_cast<double>(c->n - 1))));
+            if (K <= 0)
+                K = std::min(static_cast<int>(std::lround(std::sqrt(static_cast<double>(c->n - 1)))),
+                             (c->n - 1) / 64);
             K = std::max(1, std::min({K, W / E, (c->n - 1) / 33}));
             if (rper_sm >= q && K >= 1 && (c->n - 1) / K >= 33) {
                 if (!c->d_relay_flag) {

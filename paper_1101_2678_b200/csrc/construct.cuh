@@ -196,25 +196,47 @@ __device__ __forceinline__ void tour_tail(const ConstructParams& p, const int32_
     }
 }
 
-// Streams a growing tour to mapped (pinned) host memory 32 entries at a time:
-// lane l holds entry 32c + l of the current 32-entry chunk c; a full chunk
-// leaves as one coalesced 128-byte store over PCIe while construction goes
-// on, so the host copy costs no separate device-to-host transfer.
-// (The row address is recomputed from the kernel parameter at each flush so
-// the hot loop carries one extra register, not a pointer.)
+// Streams a growing tour to mapped (pinned) host memory 32 entries at a time
+// while construction goes on, so the host copy costs no separate
+// device-to-host transfer: when entry 32c + 31 has been written to the
+// device tour (by lane 0), the warp reads the 32-entry chunk c back from L2
+// (lane l: entry 32c + l) and stores it to the host one chunk later, as one
+// coalesced 128-byte PCIe write — nothing per step but one compare, and the
+// L2 read-back latency overlaps the next 32 steps.  (The row address is
+// recomputed from the kernel parameter, so the hot loop carries two
+// registers, not a pointer.)
 struct TourStream {
-    int held;
-    __device__ __forceinline__ void put(const ConstructParams& p, int kl, int idx, int city, int lane) {
-        if (!p.host_tours) return;
-        if (lane == (idx & 31)) held = city;
-        if ((idx & 31) == 31)
-            p.host_tours[static_cast<size_t>(kl) * (p.n + 1) + (idx & ~31) + lane] = held;
-    }
-    __device__ __forceinline__ void flush(const ConstructParams& p, int kl, int last_idx, int lane) {
-        if (!p.host_tours) return;
-        const int base = last_idx & ~31;
-        if ((last_idx & 31) != 31 && base + lane <= last_idx)
+    int held; // this lane's entry of the chunk read back, not yet stored
+    int base; // that chunk's first index, or -1
+    __device__ __forceinline__ void store(const ConstructParams& p, int kl, int lane) {
+        if (base >= 0) {
             p.host_tours[static_cast<size_t>(kl) * (p.n + 1) + base + lane] = held;
+            base = -1;
+        }
+    }
+    // after tour[idx] was written
+    __device__ __forceinline__ void put(const ConstructParams& p, const int32_t* tour, int kl, int idx,
+                                        int lane) {
+        if ((idx & 31) == 31 && p.host_tours) {
+            store(p, kl, lane);
+            __syncwarp(); // lane 0's tour stores are visible to the warp
+            held = tour[(idx & ~31) + lane];
+            base = idx & ~31;
+        }
+    }
+    // every pending chunk out (end of a run of steps)
+    __device__ __forceinline__ void drain(const ConstructParams& p, int kl, int lane) {
+        if (p.host_tours) store(p, kl, lane);
+    }
+    // after tour[last_idx] (the closing entry) was written
+    __device__ __forceinline__ void flush(const ConstructParams& p, const int32_t* tour, int kl, int last_idx,
+                                          int lane) {
+        if (!p.host_tours) return;
+        store(p, kl, lane);
+        const int b = last_idx & ~31;
+        __syncwarp();
+        if ((last_idx & 31) != 31 && b + lane <= last_idx)
+            p.host_tours[static_cast<size_t>(kl) * (p.n + 1) + b + lane] = tour[b + lane];
     }
 };
 
@@ -595,7 +617,7 @@ __device__ __forceinline__ void roulette_begin(const ConstructParams& p, Roulett
     a.tour = p.tours + static_cast<size_t>(kl) * (p.n + 1);
     a.tabu = tabu;
     a.prefetched = false;
-    a.hs = TourStream{0};
+    a.hs = TourStream{0, -1};
     tabu_init(tabu, p.tabu_words, p.n, lane);
     const int start = start_city(p, a.kg);
     __syncwarp();
@@ -603,7 +625,7 @@ __device__ __forceinline__ void roulette_begin(const ConstructParams& p, Roulett
         tabu[start >> 5] |= 1u << (start & 31);
         a.tour[0] = start;
     }
-    if (stream) a.hs.put(p, kl, 0, start, lane); // STREAM: the caller's pinned tours_out is mapped
+    if (stream) a.hs.put(p, a.tour, kl, 0, lane); // STREAM: the caller's pinned tours_out is mapped
     a.cur = start;
 }
 
@@ -612,8 +634,8 @@ __device__ __forceinline__ void roulette_end(const ConstructParams& p, RouletteA
     const int start = start_city(p, a.kg);
     if (lane == 0) a.tour[p.n] = start;
     if (stream) {
-        a.hs.put(p, a.kl, p.n, start, lane);
-        a.hs.flush(p, a.kl, p.n, lane);
+        a.hs.put(p, a.tour, a.kl, p.n, lane);
+        a.hs.flush(p, a.tour, a.kl, p.n, lane);
     }
     __syncwarp();
 }
@@ -989,7 +1011,7 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
             tabu[next >> 5] |= 1u << (next & 31);
             tour[step] = next;
         }
-        if constexpr (STREAM) hs.put(p, kl, step, next, lane);
+        if constexpr (STREAM) hs.put(p, tour, kl, step, lane);
         cur = next;
         TICK(5);
     }
@@ -1000,6 +1022,7 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
 #undef TICK
     a.cur = cur;
     a.prefetched = prefetched;
+    if constexpr (STREAM) hs.drain(p, kl, lane); // a run ends with no chunk pending
     a.hs = hs;
 }
 
@@ -1108,7 +1131,7 @@ __global__ void __launch_bounds__(32, 16) k_construct_roulette_relay(ConstructPa
                         r.tour = p.tours + static_cast<size_t>(r.kl) * (n + 1);
                         r.tabu = tabu_rel;
                         r.prefetched = false;
-                        r.hs = TourStream{0};
+                        r.hs = TourStream{0, -1};
                         const uint32_t* src = p.relay_tabu + static_cast<size_t>(rx) * p.tabu_words;
                         for (int wd = lane; wd < p.tabu_words; wd += 32) tabu_rel[wd] = __ldcg(src + wd);
                         r.cur = __ldcg(p.relay_cur + rx);
