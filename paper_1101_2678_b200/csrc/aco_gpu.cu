@@ -54,9 +54,13 @@ NcclApi& nccl() {
     static NcclApi api;
     if (!api.loaded) {
         api.loaded = true;
+        // ACO_NCCL_LIB: load another NCCL-compatible library instead (the
+        // tests' in-process loopback, tests/loopnccl, which runs several ranks
+        // on one GPU — real NCCL refuses that)
+        if (const char* lib = std::getenv("ACO_NCCL_LIB")) api.handle = dlopen(lib, RTLD_NOW | RTLD_LOCAL);
         for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-            api.handle = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
             if (api.handle) break;
+            api.handle = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
         }
         if (api.handle) {
             auto sym = [&](const char* s) { return dlsym(api.handle, s); };
