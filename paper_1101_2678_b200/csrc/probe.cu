@@ -416,3 +416,99 @@ extern "C" int aco_probe_cluster(int device, int K, int mode, int iters, double*
     *cycles_per_iter = static_cast<double>(h[0]) / iters;
     return 0;
 }
+
+// ---- TMA row copy: issue cost and completion latency of one 10 KB row as
+// K bulk copies on one mbarrier, one warp alone on the GPU (the chain the
+// latency-bound construction launches pay per step).  mode 0: issued by lane
+// 0 inside a divergent branch (as the kernel does); mode 1: the same from a
+// warp-uniform address after elect.  Per iteration: rows[i % nrows].
+__global__ void k_tma_probe(const float* __restrict__ rows, int nrows, int row_floats, int K, int mode,
+                            int iters, long long* out) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
+    float* buf = reinterpret_cast<float*>(sm + 128);
+    const int lane = threadIdx.x & 31;
+    const uint32_t sbar = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    const uint32_t sbuf = static_cast<uint32_t>(__cvta_generic_to_shared(buf));
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const uint32_t bytes = static_cast<uint32_t>(row_floats * 4);
+    const uint32_t piece = ((bytes / K) + 15u) & ~15u;
+    long long t_issue = 0, t_total = 0;
+    uint32_t phase = 0;
+    float sink = 0.f;
+    for (int it = 0; it < iters; ++it) {
+        const float* src = rows + static_cast<size_t>((it * 7919) % nrows) * row_floats;
+        __syncwarp();
+        // mode: 0 fence + expect_tx + copies; 1 expect_tx + copies (no proxy
+        // fence, as the kernel's speculative refill); 2 copies only (the
+        // expect_tx before the timed window)
+        if (mode == 2 && lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(bytes)
+                         : "memory");
+        __syncwarp();
+        const long long t0 = clock64();
+        if (lane == 0) {
+            {
+                if (mode == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                if (mode <= 1)
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(bytes)
+                                 : "memory");
+                for (uint32_t off = 0; off < bytes; off += piece) {
+                    const uint32_t b = bytes - off < piece ? bytes - off : piece;
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            sbuf + off),
+                        "l"(reinterpret_cast<const char*>(src) + off), "r"(b), "r"(sbar)
+                        : "memory");
+                }
+            }
+        }
+        __syncwarp();
+        const long long t1 = clock64();
+        asm volatile(
+            "{\n\t.reg .pred P1;\n"
+            "W_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+            "@!P1 bra W_%=;\n}" ::"r"(sbar),
+            "r"(phase)
+            : "memory");
+        phase ^= 1u;
+        sink += buf[lane * 37 % row_floats];
+        const long long t2 = clock64();
+        t_issue += t1 - t0;
+        t_total += t2 - t0;
+    }
+    if (lane == 0) {
+        out[0] = t_issue;
+        out[1] = t_total;
+        out[2] = static_cast<long long>(sink);
+    }
+}
+
+extern "C" int aco_probe_tma(int device, int row_floats, int K, int mode, int iters, double* issue_cycles,
+                             double* total_cycles) {
+    if (cudaSetDevice(device) != cudaSuccess) return 1;
+    const int nrows = 2048;
+    float* rows = nullptr;
+    long long* out = nullptr;
+    cudaMalloc(&rows, static_cast<size_t>(nrows) * row_floats * sizeof(float));
+    cudaMemset(rows, 0, static_cast<size_t>(nrows) * row_floats * sizeof(float));
+    cudaMalloc(&out, 3 * sizeof(long long));
+    const size_t smem = 128 + static_cast<size_t>(row_floats) * 4;
+    cudaFuncSetAttribute(k_tma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    // warm L2 with a first pass, then time
+    k_tma_probe<<<1, 32, smem>>>(rows, nrows, row_floats, K, mode, nrows, out);
+    k_tma_probe<<<1, 32, smem>>>(rows, nrows, row_floats, K, mode, iters, out);
+    long long h[3] = {0, 0, 0};
+    cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+    const int rc = cudaGetLastError() == cudaSuccess ? 0 : 2;
+    *issue_cycles = static_cast<double>(h[0]) / iters;
+    *total_cycles = static_cast<double>(h[1]) / iters;
+    cudaFree(rows);
+    cudaFree(out);
+    return rc;
+}
