@@ -37,9 +37,6 @@
 
 #include "philox.cuh"
 
-#ifndef ACO_LDG
-#define ACO_LDG 2 // 1: ld.global.nc.L1::no_allocate; 2: ld.global.nc (L1-allocating)
-#endif
 #ifndef ACO_SCAN_FMA
 #define ACO_SCAN_FMA 1 // warp scan levels as shfl + fma (see warp_inclusive_scan); 0: shfl + predicated add + select
 #endif
@@ -463,18 +460,6 @@ __device__ __forceinline__ int start_city(const ConstructParams& p, uint32_t kg)
     }
     return static_cast<int>(kg % static_cast<uint32_t>(p.n));
 }
-
-__device__ __forceinline__ float4 ld_stream(const float4* p) {
-#if ACO_LDG == 1
-    float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-    return v;
-#else
-    return __ldg(p);
-#endif
-}
-__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldg(p); }
 
 // ---------------------------------------------------------------------------
 // Middle certification tier: the streamed (fp32) row is still in shared
