@@ -493,6 +493,30 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
 
 bool gather_mode(const aco_gpu_ctx* c) { return c->cfg.deposit != ACO_DEP_ACCUMULATE; }
 
+// directed float roundings of a double (the host twins of __double2float_ru/rd)
+float f32_ru(double x) {
+    float f = static_cast<float>(x);
+    if (static_cast<double>(f) < x) f = std::nextafter(f, std::numeric_limits<float>::infinity());
+    return f;
+}
+float f32_rd(double x) {
+    float f = static_cast<float>(x);
+    if (static_cast<double>(f) > x) f = std::nextafter(f, -std::numeric_limits<float>::infinity());
+    return f;
+}
+
+// nn fast-path certification constants (k_construct_nn): e counts the fp32
+// quantisation (1 ulp), 5 scan levels, margins and the reference's nn
+// sequential fp64 adds; nn * 2^-149 bounds the subnormal losses; rounded
+// outward so the fp32 compares imply the exact ones
+void nn_certify_constants(ConstructParams& p, int nn) {
+    const double nn_e = (12.0 * 0x1.0p-24 + static_cast<double>(nn + 8) * 0x1.0p-53) * (1.0 + 0x1.0p-16);
+    p.nn_e32 = f32_ru(nn_e);
+    p.nn_lo32 = f32_rd(1.0 - nn_e);
+    p.nn_ce = f32_ru(nn_e + 4.0 * 0x1.0p-24);
+    p.nn_absq = static_cast<float>(nn) * 0x1.0p-149f; // exact: a subnormal multiple
+}
+
 ConstructParams make_cp(aco_gpu_ctx* c) {
     ConstructParams p{};
     p.w = c->stream_kind == ACO_STREAM_FP64 ? static_cast<const void*>(c->d_choice_p64)
@@ -529,6 +553,8 @@ ConstructParams make_cp(aco_gpu_ctx* c) {
     }
     p.S = c->S;
     p.qpos = c->d_qpos;
+    p.nn_fast32 = (c->cfg.nn <= 32 && c->d_choice_nn32 != nullptr) ? 1 : 0;
+    nn_certify_constants(p, c->cfg.nn);
     return p;
 }
 

@@ -129,6 +129,10 @@ struct ConstructParams {
     // argmax fallback), so k_deposit_nn can fold list edges into the compact
     // n x nn slot array instead of scattering over n^2 tau
     uint8_t* qpos;              // mloc x n, or null
+    // nn fast path: list weights in fp32 (nn <= 32) and its certification
+    // constants, outward-rounded on the host (nn_certify_constants)
+    int nn_fast32;
+    float nn_e32, nn_lo32, nn_ce, nn_absq;
     // Relay (k_construct_roulette_relay): the grid is relay_W = SMs x q
     // warps, warp w owns ant w; the relay_E = mloc - relay_W leftover ants are
     // each built by relay_K warps in turn, one 32-aligned segment of steps
@@ -1240,14 +1244,10 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
     uint32_t* tabu = smem_tabu;
     const int lane = threadIdx.x & 31;
     const int n = p.n, nn = p.nn;
-    // fp32 fast-path certification constants (outward-rounded): e counts the
-    // fp32 quantisation (1 ulp), 5 scan levels, margins, and the reference's
-    // nn sequential fp64 adds; nn * 2^-149 bounds the subnormal losses
-    const double nn_e = (12.0 * 0x1.0p-24 + (double)(nn + 8) * 0x1.0p-53) * (1.0 + 0x1.0p-16);
-    const float nn_e32 = __double2float_ru(nn_e);
-    const float nn_lo32 = __double2float_rd(1.0 - nn_e);
-    const float nn_ce = __double2float_ru(nn_e + 4.0 * 0x1.0p-24);
-    const float nn_absq = static_cast<float>(nn) * 0x1.0p-149f; // exact: a subnormal multiple
+    // fp32 fast-path certification constants (outward-rounded, formed on the
+    // host: nn_certify_constants) come straight from the parameter bank, so
+    // the hot loop holds no registers for them
+    const float nn_e32 = p.nn_e32, nn_lo32 = p.nn_lo32, nn_ce = p.nn_ce, nn_absq = p.nn_absq;
     for (int kl = blockIdx.x; kl < p.mloc; kl += gridDim.x) {
         const uint32_t kg = static_cast<uint32_t>(p.ant_begin + kl);
         int32_t* tour = p.tours + static_cast<size_t>(kl) * (n + 1);
@@ -1265,7 +1265,7 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
         // fp32 fast path: the current city's list (ids, scaled weights) is
         // loaded as soon as that city is chosen, one step ahead, so the L2
         // round trip overlaps the previous step's bookkeeping
-        const bool fast32 = nn <= 32 && p.choice_nn32 != nullptr;
+        const bool fast32 = p.nn_fast32 != 0; // nn <= 32 and the scaled fp32 list weights exist
         int jpre = -1;
         float wpre = 0.f;
         // SPEC: the crossing candidate's list is requested before its
@@ -1399,7 +1399,9 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                     }
                 }
             }
-            // exact sequential fold: lane q of pass k holds member 32k+q
+            // exact sequential fold (only when the fast path left the step
+            // open): lane q of pass k holds member 32k+q
+            if (next < 0 && !exhausted) {
             double acc = 0.0;
             int first_un = -1, last_pos = -1, first_un_q = 255, last_pos_q = 255;
             double mine[2] = {0.0, 0.0};
@@ -1407,7 +1409,7 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 const int q0 = 32 * k;
-                if (q0 < nn && next < 0 && !exhausted) {
+                if (q0 < nn) {
                     const int q = q0 + lane;
                     int j = -1;
                     double w = 0.0;
@@ -1441,9 +1443,7 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                     }
                 }
             }
-            if (next >= 0) {
-                // certified fast path (or its exact zero-total branch)
-            } else if (first_un >= 0) {
+            if (first_un >= 0) {
                 const double total = acc;
                 if (!(total > 0.0)) {
                     next = first_un;                                     // :89-92
@@ -1465,7 +1465,9 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                         qsel = last_pos >= 0 ? last_pos_q : first_un_q;
                     }
                 }
-            } else {
+            }
+            }
+            if (next < 0) {
                 // argmax over all unvisited, lowest index on ties (:108-120):
                 // first the row's top-K cache (k_row_topk): its first
                 // unvisited entry IS the argmax; a full scan only when every
