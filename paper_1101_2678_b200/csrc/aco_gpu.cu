@@ -553,7 +553,6 @@ ConstructParams make_cp(aco_gpu_ctx* c) {
     }
     p.S = c->S;
     p.qpos = c->d_qpos;
-    p.nn_fast32 = (c->cfg.nn <= 32 && c->d_choice_nn32 != nullptr) ? 1 : 0;
     nn_certify_constants(p, c->cfg.nn);
     return p;
 }
@@ -718,7 +717,9 @@ void launch_construct(aco_gpu_ctx* c) {
             return e ? (e[0] == '1' ? 1 : 0) : -1;
         }();
         const bool spec = spec_env >= 0 ? spec_env == 1 : c->mloc <= 12 * c->num_sms;
-        auto nnfn = spec ? k_construct_nn<true> : k_construct_nn<false>;
+        const bool f32 = c->cfg.nn <= 32 && c->d_choice_nn32 != nullptr;
+        auto nnfn = f32 ? (spec ? k_construct_nn<true, true> : k_construct_nn<false, true>)
+                        : (spec ? k_construct_nn<true, false> : k_construct_nn<false, false>);
         int per_sm = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nnfn, 32, smem1));
         const int grid = std::max(1, std::min(c->mloc, per_sm * c->num_sms));

@@ -129,9 +129,8 @@ struct ConstructParams {
     // argmax fallback), so k_deposit_nn can fold list edges into the compact
     // n x nn slot array instead of scattering over n^2 tau
     uint8_t* qpos;              // mloc x n, or null
-    // nn fast path: list weights in fp32 (nn <= 32) and its certification
+    // nn fast path (fp32 list weights, nn <= 32): its certification
     // constants, outward-rounded on the host (nn_certify_constants)
-    int nn_fast32;
     float nn_e32, nn_lo32, nn_ce, nn_absq;
     // Relay (k_construct_roulette_relay): the grid is relay_W = SMs x q
     // warps, warp w owns ant w; the relay_E = mloc - relay_W leftover ants are
@@ -1238,7 +1237,8 @@ __global__ void __launch_bounds__(32) k_construct_roulette_exact(ConstructParams
 #endif
 // SPEC: the crossing candidate's list is requested before its certification
 // (for latency-bound launches; that variant is held to 64 registers)
-template <bool SPEC>
+// FAST32: nn <= 32 with the row-scaled fp32 list weights (the fast path)
+template <bool SPEC, bool FAST32 = true>
 __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(ConstructParams p) {
     extern __shared__ uint32_t smem_tabu[];
     uint32_t* tabu = smem_tabu;
@@ -1265,7 +1265,7 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
         // fp32 fast path: the current city's list (ids, scaled weights) is
         // loaded as soon as that city is chosen, one step ahead, so the L2
         // round trip overlaps the previous step's bookkeeping
-        const bool fast32 = p.nn_fast32 != 0; // nn <= 32 and the scaled fp32 list weights exist
+        constexpr bool fast32 = FAST32;
         int jpre = -1;
         float wpre = 0.f;
         // SPEC: the crossing candidate's list is requested before its
