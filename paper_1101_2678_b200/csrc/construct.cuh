@@ -692,11 +692,10 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
 #endif
 
     for (int step = s0; step < s1; ++step) {
-        const WT* __restrict__ grow = wbase + static_cast<size_t>(cur) * p.PW;
-        if (!prefetched && lane == 0) {
+        if (!prefetched && lane == 0) { // (normally the previous step requested this row)
             fence_proxy_async_smem(); // generic reads of buf happen-before the refill
             mbar_expect_tx(bar, row_bytes);
-            tma_row(buf, grow, row_bytes, bar);
+            tma_row(buf, wbase + static_cast<size_t>(cur) * p.PW, row_bytes, bar);
         }
         // Draw 0 of steps step..step+31: lane i holds step + i (rng.hpp:74-80).
         if (((step - 1) & 31) == 0)
