@@ -419,7 +419,26 @@ __device__ __forceinline__ float scan_up_add(float v, int off) {
         : "f"(v), "r"(off));
     return y;
 }
+// in-place form: the source-lane predicate of shfl.up guards an add into v
+// itself — two dependent instructions per level, no select, no mask registers
+__device__ __forceinline__ void scan_up_add_inplace(float& v, int off) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .f32 y;\n\t"
+        "shfl.sync.up.b32 y|p, %0, %1, 0, -1;\n\t"
+        "@p add.rn.f32 %0, %0, y;\n}"
+        : "+f"(v)
+        : "r"(off));
+}
+// INPLACE: the predicated in-place form (fewer instructions: pays at high
+// occupancy, where issue slots are scarce; the fma form's shorter chain pays
+// in latency-bound launches)
+template <bool INPLACE = false>
 __device__ __forceinline__ float warp_inclusive_scan(float v) {
+    if constexpr (INPLACE) {
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) scan_up_add_inplace(v, off);
+        return v;
+    }
 #if ACO_SCAN_FMA
     // two dependent instructions per level instead of three: with m = 1 for
     // lanes >= off (else 0), fma(y, m, v) is fl(v + y) or exactly v — the
@@ -630,7 +649,7 @@ __device__ __forceinline__ void roulette_end(const ConstructParams& p, RouletteA
 
 // Steps [s0, s1) of one ant.  smem: the kernel's dynamic shared memory
 // (mbarrier, row buffer, own tabu, chunk_start, gsum).
-template <typename WT, int NV, int MAXR, bool STREAM>
+template <typename WT, int NV, int MAXR, bool STREAM, bool SCAN_INPLACE = false>
 __device__ __forceinline__ void roulette_steps(const ConstructParams& p, RouletteAnt& a, int s0, int s1,
                                                unsigned char* smem_raw, uint32_t& phase,
                                                unsigned long long& fb, unsigned long long& fb2) {
@@ -764,7 +783,7 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
                 AT d = static_cast<AT>(tree_sum<WT, NG>(gs));
                 TICK(0);
                 if constexpr (F32) {
-                    d = warp_inclusive_scan(d);
+                    d = warp_inclusive_scan<SCAN_INPLACE>(d);
                 } else {
 #pragma unroll
                     for (int off = 1; off < 32; off <<= 1) {
@@ -1155,7 +1174,7 @@ __global__ void __launch_bounds__(32, 16) k_construct_roulette_relay(ConstructPa
         } else {
             stage = 2;
         }
-        roulette_steps<float, NV, 1, STREAM>(p, ants[which], s0, s1, smem_raw, phase, fb, fb2);
+        roulette_steps<float, NV, 1, STREAM, true>(p, ants[which], s0, s1, smem_raw, phase, fb, fb2);
         if (which == 0) s = s1;
     }
     roulette_end(p, ants[0], lane, STREAM);
@@ -1313,7 +1332,7 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                 if (!unb) {
                     exhausted = true;
                 } else {
-                    const float P = warp_inclusive_scan(w);
+                    const float P = warp_inclusive_scan<!SPEC>(w);
                     const float T = __shfl_sync(kFull, P, 31);
                     const float Eu = __shfl_up_sync(kFull, P, 1); // every lane shuffles
                     const float E = lane == 0 ? 0.f : Eu;
