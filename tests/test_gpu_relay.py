@@ -32,9 +32,12 @@ def engine(aco, n, m, deposit=3, random_start=False, seed=1):
     return prob, aco.Engine(prob, cfg)
 
 
-@pytest.mark.parametrize("n,extra,random_start", [(600, 5, False), (1200, 3, True), (700, 1, False)])
-def test_relay_multi_iteration_bit_exact(aco, oracle, n, extra, random_start):
-    m = 4 * sms() + extra
+@pytest.mark.parametrize("n,q,extra,random_start", [(600, 4, 5, False), (1200, 4, 3, True), (700, 4, 1, False),
+                                                     (200, 4, 3, False), (300, 12, 5, True)])
+def test_relay_multi_iteration_bit_exact(aco, oracle, n, q, extra, random_start):
+    """q = 12 warps per SM also forms the tour lengths, 1/C_k and the gather's
+    succ/pred in the relay kernel's fused tail (checked through tau)."""
+    m = q * sms() + extra
     prob, eng = engine(aco, n, m, random_start=random_start)
     with eng:
         tau = np.full((n, n), eng.tau0)
