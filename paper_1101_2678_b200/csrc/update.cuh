@@ -573,8 +573,11 @@ __device__ __forceinline__ double tau_pow(double t, double alpha, const LibmPowT
 // when something needs the finished row: the gather fold, the permuted
 // streamed copies (row max first) and the nn weights; otherwise the kernel
 // runs with no dynamic shared memory and full occupancy.
+// CTAs per SM the register budget must allow: 4 for the choice pass (the
+// one-GPU update: pr2392 -3%, 10k -5.5%, 64 registers), 3 for the others
+// (the delta pass at 64 registers was 9% slower)
 template <int MODE>
-__global__ void __launch_bounds__(256, 3) k_rows(RowParams p) {
+__global__ void __launch_bounds__(256, MODE == MODE_CHOICE ? 4 : 3) k_rows(RowParams p) {
     extern __shared__ double rowbuf[]; // P64 doubles when use_row
     __shared__ double s_max[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
