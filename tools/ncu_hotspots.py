@@ -26,3 +26,10 @@ tot = sum(int(r[iW]) for r in data) or 1
 print("total stall samples", tot, "instructions", sum(int(r[iE]) for r in data))
 for r in sorted(data, key=lambda r: -int(r[iW]))[:N]:
     print(f"{100*int(r[iW])/tot:5.1f}% exec={int(r[iE]):>10d} {r[iS].strip()[:80]}")
+agg = {}
+for r in data:
+    for i, x in enumerate(hdr):
+        if x.startswith("stall_") and "Not Issued" not in x:
+            agg[x[6:]] = agg.get(x[6:], 0.0) + float(r[i] or 0)
+print("stall reasons (% of samples):",
+      ", ".join(f"{k} {100 * v / tot:.1f}" for k, v in sorted(agg.items(), key=lambda kv: -kv[1])[:8]))
