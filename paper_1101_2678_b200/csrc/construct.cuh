@@ -1260,6 +1260,7 @@ template <bool SPEC, bool FAST32 = true>
 __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(ConstructParams p) {
     extern __shared__ uint32_t smem_tabu[];
     uint32_t* tabu = smem_tabu;
+
     const int lane = threadIdx.x & 31;
     const int n = p.n, nn = p.nn;
     // fp32 fast-path certification constants (outward-rounded, formed on the
@@ -1280,6 +1281,7 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
         int cur = start;
         unsigned long long fb = 0, fb_full = 0;
         double ubatch = 0.0;
+        float ub_up = 0.f, ub_dn = 0.f;
         // fp32 fast path: the current city's list (ids, scaled weights) is
         // loaded as soon as that city is chosen, one step ahead, so the L2
         // round trip overlaps the previous step's bookkeeping
@@ -1299,11 +1301,19 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
             const double* __restrict__ row = p.w64 + static_cast<size_t>(cur) * p.P64;
             const int32_t* nb = p.nn_lists + static_cast<size_t>(cur) * nn;
             const double* wn = p.choice_nn + static_cast<size_t>(cur) * nn;
-            if (((step - 1) & 31) == 0)
+            // Draw 0 of steps step..step+31: lane i holds step + i
+            // (rng.hpp:74-80), kept in fp64 and as the float pair that
+            // brackets it (rounded down / up): the fast path broadcasts the
+            // pair (two 32-bit shuffles, no conversions per step), the exact
+            // paths the fp64 draw
+            if (((step - 1) & 31) == 0) {
                 ubatch = philox_uniform(p.seed, p.iteration, kg,
                                         static_cast<uint32_t>(step + lane), 0);
-            const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
-            const float u_up = __double2float_ru(u), u_dn = __double2float_rd(u);
+                ub_up = __double2float_ru(ubatch);
+                ub_dn = __double2float_rd(ubatch);
+            }
+            const float u_up = __shfl_sync(kFull, ub_up, (step - 1) & 31);
+            const float u_dn = __shfl_sync(kFull, ub_dn, (step - 1) & 31);
             int next = -1;
             int qsel = 255;         // list position of next (255: not from the list)
             bool exhausted = false; // every list member visited: argmax fallback
@@ -1336,7 +1346,9 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                     const float T = __shfl_sync(kFull, P, 31);
                     const float Eu = __shfl_up_sync(kFull, P, 1); // every lane shuffles
                     const float E = lane == 0 ? 0.f : Eu;
-                    const float t32 = __fmul_rn(__double2float_rn(u), T);
+                    // the candidate threshold only (the certification
+                    // below brackets u between u_dn and u_up)
+                    const float t32 = __fmul_rn(u_dn, T);
                     const unsigned cr = __ballot_sync(kFull, q < nn && w > 0.f && P > t32 && T > 0.f);
                     if (cr) {
                         const int J = __ffs(cr) - 1;
@@ -1365,6 +1377,7 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                     }
                 }
             } else if (nn <= 32) {
+                const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
                 // Fast path: one fp64 warp scan instead of the sequential
                 // fold, then CERTIFY the crossing against the reference's
                 // sequential sums (as in k_construct_roulette): every scan
@@ -1420,6 +1433,7 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
             // exact sequential fold (only when the fast path left the step
             // open): lane q of pass k holds member 32k+q
             if (next < 0 && !exhausted) {
+            const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
             double acc = 0.0;
             int first_un = -1, last_pos = -1, first_un_q = 255, last_pos_q = 255;
             double mine[2] = {0.0, 0.0};
