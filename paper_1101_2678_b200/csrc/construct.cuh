@@ -1251,7 +1251,7 @@ __global__ void __launch_bounds__(32) k_construct_roulette_exact(ConstructParams
 // (construction.hpp:108-120), which consumes no draw; it streams the fp64
 // row with 8 independent 16-byte loads per lane in flight.
 #ifndef ACO_NN_MINB
-#define ACO_NN_MINB 16 // resident warps per SM the register budget must allow
+#define ACO_NN_MINB 28 // resident warps per SM the register budget must allow
 #endif
 // SPEC: the crossing candidate's list is requested before its certification
 // (for latency-bound launches; that variant is held to 64 registers)
@@ -1293,6 +1293,12 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
         int jg = -1;
         int jspec = -1;
         float wspec = 0.f;
+        // kHold (full-occupancy launches): the open 32-entry chunk of the
+        // tour (and of the list positions) is held in the lanes — lane
+        // (s & 31) holds tour[s] / qpos[s-1] — and stored coalesced when the
+        // chunk closes, instead of lane 0 storing every step
+        constexpr bool kHold = !SPEC;
+        int held_t = 0, held_q = 0;
         if (fast32 && lane < nn) {
             jpre = p.nn_lists[static_cast<size_t>(start) * nn + lane];
             wpre = p.choice_nn32[static_cast<size_t>(start) * nn + lane];
@@ -1518,21 +1524,9 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                             if (b && next < 0) next = __shfl_sync(kFull, ids[r], __ffs(b) - 1);
                         }
                     }
-                    if (next >= 0) {
-                        if (fast32 && lane < nn && step + 1 < n) {
-                            jpre = p.nn_lists[static_cast<size_t>(next) * nn + lane];
-                            wpre = p.choice_nn32[static_cast<size_t>(next) * nn + lane];
-                        }
-                        if (lane == 0) {
-                            tabu[next >> 5] |= 1u << (next & 31);
-                            tour[step] = next;
-                            if (p.qpos) p.qpos[static_cast<size_t>(kl) * n + step - 1] = 255;
-                        }
-                        __syncwarp();
-                        cur = next;
-                        continue;
-                    }
+                    if (next >= 0) qsel = 255; // not from the list
                 }
+                if (next < 0) {
                 ++fb_full;
                 double bw = -1.0;
                 int bj = -1;
@@ -1583,6 +1577,7 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                     if (oj >= 0 && (bj < 0 || ow > bw || (ow == bw && oj < bj))) { bw = ow; bj = oj; }
                 }
                 next = bj;
+                }
             }
             if (fast32 && step + 1 < n) {
                 if (SPEC && next == jg) { // the speculated list is the one
@@ -1594,7 +1589,20 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                 }
             }
             jg = -1;
-            if (lane == 0) {
+            if constexpr (kHold) {
+                if (lane == 0) tabu[next >> 5] |= 1u << (next & 31);
+                if (lane == (step & 31)) {
+                    held_t = next;
+                    held_q = qsel;
+                }
+                if ((step & 31) == 31 || step == n - 1) {
+                    const int s = (step & ~31) + lane;
+                    if (s >= 1 && s <= step) {
+                        tour[s] = held_t;
+                        if (p.qpos) p.qpos[static_cast<size_t>(kl) * n + s - 1] = static_cast<uint8_t>(held_q);
+                    }
+                }
+            } else if (lane == 0) {
                 tabu[next >> 5] |= 1u << (next & 31);
                 tour[step] = next;
                 if (p.qpos) p.qpos[static_cast<size_t>(kl) * n + step - 1] = static_cast<uint8_t>(qsel);
