@@ -1789,7 +1789,8 @@ aco_status aco_gpu_iterate(aco_gpu_ctx* c, aco_gpu_iter_record* rec, int32_t* to
         aco_gpu_iter_record* r = rec ? rec : &tmp;
         fill_common(c, r);
         // The one-warp-per-ant roulette streams each tour into a pinned,
-        // device-mapped tours_out while it is built (TourStream); otherwise
+        // device-mapped tours_out while it is built (32-entry chunks held in
+        // the lanes, stored as each chunk closes); otherwise
         // the tours are copied after the construction.
         c->host_tours = nullptr;
         if (tours_out && c->cfg.selection == ACO_SEL_ROULETTE && !c->exact_only &&

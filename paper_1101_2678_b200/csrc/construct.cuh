@@ -196,50 +196,6 @@ __device__ __forceinline__ void tour_tail(const ConstructParams& p, const int32_
     }
 }
 
-// Streams a growing tour to mapped (pinned) host memory 32 entries at a time
-// while construction goes on, so the host copy costs no separate
-// device-to-host transfer: when entry 32c + 31 has been written to the
-// device tour (by lane 0), the warp reads the 32-entry chunk c back from L2
-// (lane l: entry 32c + l) and stores it to the host one chunk later, as one
-// coalesced 128-byte PCIe write — nothing per step but one compare, and the
-// L2 read-back latency overlaps the next 32 steps.  (The row address is
-// recomputed from the kernel parameter, so the hot loop carries two
-// registers, not a pointer.)
-struct TourStream {
-    int held; // this lane's entry of the chunk read back, not yet stored
-    int base; // that chunk's first index, or -1
-    __device__ __forceinline__ void store(const ConstructParams& p, int kl, int lane) {
-        if (base >= 0) {
-            p.host_tours[static_cast<size_t>(kl) * (p.n + 1) + base + lane] = held;
-            base = -1;
-        }
-    }
-    // after tour[idx] was written
-    __device__ __forceinline__ void put(const ConstructParams& p, const int32_t* tour, int kl, int idx,
-                                        int lane) {
-        if ((idx & 31) == 31 && p.host_tours) {
-            store(p, kl, lane);
-            __syncwarp(); // lane 0's tour stores are visible to the warp
-            held = tour[(idx & ~31) + lane];
-            base = idx & ~31;
-        }
-    }
-    // every pending chunk out (end of a run of steps)
-    __device__ __forceinline__ void drain(const ConstructParams& p, int kl, int lane) {
-        if (p.host_tours) store(p, kl, lane);
-    }
-    // after tour[last_idx] (the closing entry) was written
-    __device__ __forceinline__ void flush(const ConstructParams& p, const int32_t* tour, int kl, int last_idx,
-                                          int lane) {
-        if (!p.host_tours) return;
-        store(p, kl, lane);
-        const int b = last_idx & ~31;
-        __syncwarp();
-        if ((last_idx & 31) != 31 && b + lane <= last_idx)
-            p.host_tours[static_cast<size_t>(kl) * (p.n + 1) + b + lane] = tour[b + lane];
-    }
-};
-
 __device__ __forceinline__ bool tabu_test(const uint32_t* tabu, int j) {
     return (tabu[j >> 5] >> (j & 31)) & 1u;
 }
@@ -613,7 +569,6 @@ struct RouletteAnt {
     uint32_t* tabu;   // shared-memory tabu bitmask
     int cur;          // current city
     bool prefetched;  // the row of `cur` is already requested (speculative TMA)
-    TourStream hs;    // STREAM: the partial 32-entry chunk
 };
 
 // Lays the ant's start city down (tabu, tour[0]).
@@ -624,7 +579,6 @@ __device__ __forceinline__ void roulette_begin(const ConstructParams& p, Roulett
     a.tour = p.tours + static_cast<size_t>(kl) * (p.n + 1);
     a.tabu = tabu;
     a.prefetched = false;
-    a.hs = TourStream{0, -1};
     tabu_init(tabu, p.tabu_words, p.n, lane);
     const int start = start_city(p, a.kg);
     __syncwarp();
@@ -632,17 +586,16 @@ __device__ __forceinline__ void roulette_begin(const ConstructParams& p, Roulett
         tabu[start >> 5] |= 1u << (start & 31);
         a.tour[0] = start;
     }
-    if (stream) a.hs.put(p, a.tour, kl, 0, lane); // STREAM: the caller's pinned tours_out is mapped
+    if (stream && lane == 0) p.host_tours[static_cast<size_t>(kl) * (p.n + 1)] = start; // mapped tours_out
     a.cur = start;
 }
 
 // Closes the tour (tour[n] = start).
 __device__ __forceinline__ void roulette_end(const ConstructParams& p, RouletteAnt& a, int lane, bool stream) {
     const int start = start_city(p, a.kg);
-    if (lane == 0) a.tour[p.n] = start;
-    if (stream) {
-        a.hs.put(p, a.tour, a.kl, p.n, lane);
-        a.hs.flush(p, a.tour, a.kl, p.n, lane);
+    if (lane == 0) {
+        a.tour[p.n] = start;
+        if (stream) p.host_tours[static_cast<size_t>(a.kl) * (p.n + 1) + p.n] = start;
     }
     __syncwarp();
 }
@@ -696,7 +649,12 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
     uint32_t* const tabu = a.tabu;
     int cur = a.cur;
     bool prefetched = a.prefetched;
-    TourStream hs = a.hs;
+    // STREAM: lane (s & 31) holds tour[s] of the open 32-entry chunk; the
+    // chunk is stored when it closes (or the run ends), to the device tour
+    // and to the caller's mapped pinned tours_out alike — one coalesced
+    // 128-byte write each, no per-step store and no read-back.  (Without a
+    // host buffer lane 0 stores every step: measured no slower there.)
+    int held = 0;
     // Draw 0 of steps b..b+31 (b = 1 mod 32): lane i holds step b + i
     // (rng.hpp:74-80); a run starting inside a batch draws it first.
     double ubatch = 0.0;
@@ -1013,11 +971,20 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
         // ballot/shuffle, so lane 0 updates it without a barrier; the
         // __syncwarp before the next step's mbarrier wait orders it before
         // any later read.
-        if (lane == 0) {
+        if constexpr (STREAM) {
+            if (lane == 0) tabu[next >> 5] |= 1u << (next & 31);
+            if (lane == (step & 31)) held = next;
+            if ((step & 31) == 31 || step == s1 - 1) { // the chunk (or the run) closes
+                const int s = (step & ~31) + lane;
+                if (s >= s0 && s <= step) {
+                    tour[s] = held;
+                    p.host_tours[static_cast<size_t>(kl) * (n + 1) + s] = held;
+                }
+            }
+        } else if (lane == 0) {
             tabu[next >> 5] |= 1u << (next & 31);
             tour[step] = next;
         }
-        if constexpr (STREAM) hs.put(p, tour, kl, step, lane);
         cur = next;
         TICK(5);
     }
@@ -1028,8 +995,6 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
 #undef TICK
     a.cur = cur;
     a.prefetched = prefetched;
-    if constexpr (STREAM) hs.drain(p, kl, lane); // a run ends with no chunk pending
-    a.hs = hs;
 }
 
 template <typename WT, int NV, int MAXR, bool STREAM = false>
@@ -1137,7 +1102,6 @@ __global__ void __launch_bounds__(32, 16) k_construct_roulette_relay(ConstructPa
                         r.tour = p.tours + static_cast<size_t>(r.kl) * (n + 1);
                         r.tabu = tabu_rel;
                         r.prefetched = false;
-                        r.hs = TourStream{0, -1};
                         const uint32_t* src = p.relay_tabu + static_cast<size_t>(rx) * p.tabu_words;
                         for (int wd = lane; wd < p.tabu_words; wd += 32) tabu_rel[wd] = __ldcg(src + wd);
                         r.cur = __ldcg(p.relay_cur + rx);

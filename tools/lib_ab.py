@@ -11,7 +11,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CHILD = r"""
-import sys, json, statistics, hashlib
+import os, sys, json, statistics, hashlib
 sys.path.insert(0, %r)
 from paper_1101_2678_b200 import aco
 n, m, sel, G = %d, %d, %d, %d
@@ -20,9 +20,15 @@ cfg = aco.RunConfig(params=aco.Parameters(m=m, seed=1),
                     selection=aco.SelectionStrategy(aco.Selection(sel)), world=G, rank=0)
 h = hashlib.sha256()
 with aco.Engine(prob, cfg) as e:
+    kw = {}
+    if os.environ.get("LIB_AB_PINNED") == "1":  # tours streamed into pinned host memory
+        import torch
+        mloc = e.ant_end - e.ant_begin
+        kw = dict(tours_out=torch.empty((mloc, n + 1), dtype=torch.int32, pin_memory=True).numpy(),
+                  lengths_out=torch.empty(mloc, dtype=torch.int64, pin_memory=True).numpy())
     recs = []
     for i in range(7):
-        recs.append(e.run_iteration())
+        recs.append(e.run_iteration(**kw))
         h.update(e.ants()[0].tobytes())
     recs = recs[2:]
     print(json.dumps({"kernel_ms": round(statistics.median(r.construct_kernel_ms for r in recs), 4),
