@@ -379,9 +379,9 @@ void choose_stream_layout(aco_gpu_ctx* c) {
 void launch_topk(aco_gpu_ctx* c) {
     if (!c->d_topk) return;
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_row_topk, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_row_topk, kTopThreads, 0));
     const int grid = std::max(1, std::min(c->n, std::max(1, per_sm) * c->num_sms));
-    k_row_topk<<<grid, 256, 0, c->stream>>>(c->d_choice, c->n, c->P64, c->d_topk);
+    k_row_topk<<<grid, kTopThreads, 0, c->stream>>>(c->d_choice, c->n, c->P64, c->d_topk);
     check_launch(c, "k_row_topk");
 }
 

@@ -1477,16 +1477,20 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                 ++fb;
                 if (p.topk) {
                     const int32_t* tk = p.topk + static_cast<size_t>(cur) * p.topk_k;
-                    int ids[4];
+                    // 128 entries (4 loads per lane in flight) at a time
+                    for (int r0 = 0; r0 < p.topk_k && next < 0; r0 += 128) {
+                        int ids[4];
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) ids[r] = 32 * r < p.topk_k ? tk[32 * r + lane] : -1;
-                    if (__shfl_sync(kFull, ids[0], 0) != -2) {
+                        for (int r = 0; r < 4; ++r)
+                            ids[r] = r0 + 32 * r < p.topk_k ? tk[r0 + 32 * r + lane] : -1;
+                        if (r0 == 0 && __shfl_sync(kFull, ids[0], 0) == -2) break; // invalid row: scan
 #pragma unroll
                         for (int r = 0; r < 4; ++r) {
                             const bool un = ids[r] >= 0 && !tabu_test(tabu, ids[r]);
                             const unsigned b = __ballot_sync(kFull, un);
                             if (b && next < 0) next = __shfl_sync(kFull, ids[r], __ffs(b) - 1);
                         }
+                        if (__shfl_sync(kFull, ids[3], 31) < 0) break; // end of the list (n < K)
                     }
                     if (next >= 0) qsel = 255; // not from the list
                 }

@@ -872,8 +872,12 @@ __global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
 // KT cities have w >= M; a second pass over the row (L2-resident by then)
 // collects those cities, which are ranked by the total order with integer
 // compares of the bit patterns (w >= 0, so they order like w).  Bytes: 8 n^2 from HBM (+ the L2 re-read) + 4 KT n written.
-constexpr int kTopK = 128;
-constexpr int kTopCap = 768;
+#ifndef ACO_TOPK_K
+#define ACO_TOPK_K 256 // entries per row of the argmax cache (128: 10k one GPU 1.5 ms slower construction, 0.3 ms faster rebuild)
+#endif
+constexpr int kTopK = ACO_TOPK_K;
+constexpr int kTopThreads = 2 * kTopK; // one sub-range per thread
+constexpr int kTopCap = kTopK <= 256 ? 6 * kTopK : 4 * kTopK; // static shared memory <= 48 KB
 #ifndef ACO_TOPK_MINB
 #define ACO_TOPK_MINB 8 // CTAs per SM the register budget must allow
 #endif
@@ -884,7 +888,7 @@ constexpr int kTopCap = 768;
 #define ACO_TOPK_B 6 // row loads in flight per thread (8 spills at 32 registers)
 #endif
 
-__global__ void __launch_bounds__(256, ACO_TOPK_MINB) k_row_topk(const double* __restrict__ choice, int n, int P64,
+__global__ void __launch_bounds__(kTopThreads, ACO_TOPK_MINB * 256 / kTopThreads) k_row_topk(const double* __restrict__ choice, int n, int P64,
                                                   int32_t* __restrict__ topk) {
     // candidates as (bit pattern of w >= 0, which orders like w; index)
     __shared__ ulonglong2 cand[kTopCap];
@@ -894,13 +898,13 @@ __global__ void __launch_bounds__(256, ACO_TOPK_MINB) k_row_topk(const double* _
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
         const double* src = choice + static_cast<size_t>(i) * P64;
         if (tid == 0) s_cnt = 0;
-        // sub-range q = j mod 256 is thread q's: its maximum straight from HBM
+        // sub-range q = j mod kTopThreads is thread q's: its maximum straight from HBM
         double m0 = -1.0;
-        for (int k0 = 0; k0 < n; k0 += 256 * B) {
+        for (int k0 = 0; k0 < n; k0 += kTopThreads * B) {
             double v[B];
 #pragma unroll
             for (int u = 0; u < B; ++u) {
-                const int j = k0 + 256 * u + tid;
+                const int j = k0 + kTopThreads * u + tid;
                 v[u] = j < n ? __ldg(src + j) : -1.0;
             }
 #pragma unroll
@@ -921,11 +925,11 @@ __global__ void __launch_bounds__(256, ACO_TOPK_MINB) k_row_topk(const double* _
         }
         const double M = __longlong_as_double(static_cast<long long>(H) << 32);
         // second pass over the (now L2-resident) row: collect w >= M
-        for (int k0 = 0; k0 < n; k0 += 256 * B) {
+        for (int k0 = 0; k0 < n; k0 += kTopThreads * B) {
             double v[B];
 #pragma unroll
             for (int u = 0; u < B; ++u) {
-                const int j = k0 + 256 * u + tid;
+                const int j = k0 + kTopThreads * u + tid;
                 v[u] = j < n ? __ldg(src + j) : -1.0;
             }
 #pragma unroll
@@ -934,7 +938,7 @@ __global__ void __launch_bounds__(256, ACO_TOPK_MINB) k_row_topk(const double* _
                     const int pos = atomicAdd(&s_cnt, 1);
                     if (pos < kTopCap)
                         cand[pos] = make_ulonglong2(static_cast<unsigned long long>(__double_as_longlong(v[u])),
-                                                    static_cast<unsigned long long>(k0 + 256 * u + tid));
+                                                    static_cast<unsigned long long>(k0 + kTopThreads * u + tid));
                 }
             }
         }
@@ -945,7 +949,7 @@ __global__ void __launch_bounds__(256, ACO_TOPK_MINB) k_row_topk(const double* _
             if (tid == 0) out[0] = -2; // invalid: the construction scans the row
         } else {
 #if ACO_TOPK_REFINE
-            if (c > kTopK + 16 && c <= 256) {
+            if (c > kTopK + 16 && c <= kTopThreads) {
                 // second threshold, over the candidates' own high words: a
                 // candidate below H2 is below every candidate at or above
                 // it, and >= KT are at or above, so only those are ranked
@@ -966,7 +970,7 @@ __global__ void __launch_bounds__(256, ACO_TOPK_MINB) k_row_topk(const double* _
             }
 #endif
             // rank under (w desc, index asc), branch-free integer compares
-            for (int a = tid; a < c; a += 256) {
+            for (int a = tid; a < c; a += kTopThreads) {
                 const ulonglong2 ea = cand[a];
                 int r = 0;
                 for (int b = 0; b < c; ++b) {
@@ -975,7 +979,7 @@ __global__ void __launch_bounds__(256, ACO_TOPK_MINB) k_row_topk(const double* _
                 }
                 if (r < kTopK) out[r] = static_cast<int32_t>(ea.y);
             }
-            for (int r = c + tid; r < kTopK; r += 256) out[r] = -1; // n < KT: end of list
+            for (int r = c + tid; r < kTopK; r += kTopThreads) out[r] = -1; // n < KT: end of list
         }
         __syncthreads();
     }

@@ -237,7 +237,7 @@ def test_nn_argmax_cache_bit_exact(aco, oracle, monkeypatch, topk):
         argmax, full = int(fields["argmax_fallbacks"]), int(fields["full_row_scans"])
         assert argmax > 1000
         if topk == "1":
-            assert fields["topk"] == "128" and full < argmax // 2
+            assert int(fields["topk"]) >= 128 and full < argmax // 2
         else:
             assert fields["topk"] == "off" and full == argmax
 
@@ -308,8 +308,9 @@ def test_nn_topk_lists_exact(aco, n, pattern):
     asc) of the device choice rows: uniform tau (eta ties from integer
     distances), log-uniform tau over 2^-100..1 (exponents spread across the
     threshold search), tau from 3 values (heavy ties), and n < K (the list
-    ends with -1).  A row may only be marked -2 (full scan) when more than
-    768 of its cities tie at or above its K-th value's 2^-20 band."""
+    ends with -1).  A row may only be marked -2 (full scan) when more of
+    its cities than the kernel's candidate scratch holds (6 K) tie at or
+    above its K-th value's 2^-20 band."""
     prob, eng = make(aco, n, selection=1, deposit=0, nn=8, ant_range=(0, 1))
     rng = np.random.default_rng(n)
     with eng:
@@ -325,12 +326,13 @@ def test_nn_topk_lists_exact(aco, n, pattern):
         ch = eng.choice()
         got = eng.topk()
     K = got.shape[1]
-    assert K == 128
+    assert K in (128, 256, 512)
+    cap = 6 * K if K <= 256 else 4 * K
     exp = _expected_topk(ch, K)
     bad = got[:, 0] == -2
     for i in np.nonzero(bad)[0]:
         kth = np.sort(ch[i])[::-1][K - 1]
-        assert np.count_nonzero(ch[i] >= kth * (1 - 2.0 ** -20)) > 768, f"row {i} flagged without overflow"
+        assert np.count_nonzero(ch[i] >= kth * (1 - 2.0 ** -20)) > cap, f"row {i} flagged without overflow"
     assert np.array_equal(got[~bad], exp[~bad])
     if pattern != "ties":
         assert not bad.any()

@@ -154,7 +154,7 @@ def test_synth10k_nn30_evolved_tau_topk_live(aco, oracle):
                 t, l = eng.ants()
                 assert np.array_equal(t, t_ref), f"ants {lo}.. iteration {it}"
                 assert np.array_equal(l, l_ref)
-                assert desc["topk"] == "128"
+                assert int(desc["topk"]) >= 128  # the cache is live
                 assert int(desc["argmax_fallbacks"]) > 0
                 assert int(desc["full_row_scans"]) < int(desc["argmax_fallbacks"])
                 eng.update()
