@@ -888,11 +888,69 @@ constexpr int kTopCap = kTopK <= 256 ? 6 * kTopK : 4 * kTopK; // static shared m
 #define ACO_TOPK_B 6 // row loads in flight per thread (8 spills at 32 registers)
 #endif
 
+// The K-th largest of the valid v (one per thread of an NT-thread block), 0
+// when fewer than K are valid: 8-bit radix select, most significant digit
+// first — per digit one shared histogram of the values still matching the
+// prefix and one warp locating the digit where the count from the top
+// reaches k (9 block barriers instead of a 31-step bitwise search).
+// hist: 2 x 256 ints, sel: 2 ints of shared memory.
+template <int NT>
+__device__ __forceinline__ uint32_t block_kth_largest(uint32_t v, bool valid, int K, int* hist, int* sel) {
+    const int tid = threadIdx.x;
+    for (int b = tid; b < 256; b += NT) hist[b] = 0;
+    if (__syncthreads_count(valid) < K) return 0u;
+    uint32_t prefix = 0, mask = 0;
+    int k = K;
+#pragma unroll 1
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        int* h = hist + (pass & 1) * 256;
+        if (valid && (v & mask) == prefix) atomicAdd(&h[(v >> shift) & 255u], 1);
+        __syncthreads();
+        if (tid >= 32) { // the other buffer was last read in the previous pass
+            int* h2 = hist + ((pass + 1) & 1) * 256;
+            for (int b = tid - 32; b < 256; b += NT - 32) h2[b] = 0;
+        } else {
+            int c[8], sum = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                c[q] = h[255 - 8 * tid - q]; // descending digits
+                sum += c[q];
+            }
+            int incl = sum;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, off);
+                if (tid >= off) incl += y;
+            }
+            const int excl = incl - sum;
+            if (excl < k && k <= incl) {
+                int acc = excl;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (acc < k && acc + c[q] >= k) {
+                        sel[0] = 255 - 8 * tid - q;
+                        sel[1] = k - acc;
+                    }
+                    acc += c[q];
+                }
+            }
+        }
+        __syncthreads();
+        prefix |= static_cast<uint32_t>(sel[0]) << shift;
+        mask |= 255u << shift;
+        k = sel[1];
+    }
+    return prefix;
+}
+
 __global__ void __launch_bounds__(kTopThreads, ACO_TOPK_MINB * 256 / kTopThreads) k_row_topk(const double* __restrict__ choice, int n, int P64,
                                                   int32_t* __restrict__ topk) {
     // candidates as (bit pattern of w >= 0, which orders like w; index)
     __shared__ ulonglong2 cand[kTopCap];
     __shared__ int s_cnt;
+    __shared__ int s_hist[512];
+    __shared__ int s_sel[2];
     const int tid = threadIdx.x;
     constexpr int B = ACO_TOPK_B;
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
@@ -917,12 +975,8 @@ __global__ void __launch_bounds__(kTopThreads, ACO_TOPK_MINB * 256 / kTopThreads
         // i.e. n < KT: M = 0 and every city is a candidate.)
         const bool valid = m0 >= 0.0;
         const uint32_t hi = valid ? static_cast<uint32_t>(__double_as_longlong(m0) >> 32) : 0u;
-        uint32_t H = 0;
-#pragma unroll 1
-        for (int bit = 30; bit >= 0; --bit) {
-            const uint32_t c = H | (1u << bit);
-            if (__syncthreads_count(valid && hi >= c) >= kTopK) H = c;
-        }
+        // (the K-th largest high word is exactly that H)
+        const uint32_t H = block_kth_largest<kTopThreads>(hi, valid, kTopK, s_hist, s_sel);
         const double M = __longlong_as_double(static_cast<long long>(H) << 32);
         // second pass over the (now L2-resident) row: collect w >= M
         for (int k0 = 0; k0 < n; k0 += kTopThreads * B) {
@@ -956,12 +1010,7 @@ __global__ void __launch_bounds__(kTopThreads, ACO_TOPK_MINB * 256 / kTopThreads
                 const bool own = tid < c;
                 const ulonglong2 e = own ? cand[tid] : make_ulonglong2(0ull, 0ull);
                 const uint32_t h = static_cast<uint32_t>(e.x >> 32);
-                uint32_t H2 = 0;
-#pragma unroll 1
-                for (int bit = 30; bit >= 0; --bit) {
-                    const uint32_t cnd = H2 | (1u << bit);
-                    if (__syncthreads_count(own && h >= cnd) >= kTopK) H2 = cnd;
-                }
+                const uint32_t H2 = block_kth_largest<kTopThreads>(h, own, kTopK, s_hist, s_sel);
                 if (tid == 0) s_cnt = 0;
                 __syncthreads();
                 if (own && h >= H2) cand[atomicAdd(&s_cnt, 1)] = e;
