@@ -306,38 +306,50 @@ __global__ void k_fill(double* p, size_t count, double v) {
 using ConstructFn = void (*)(ConstructParams);
 
 // the relay variant (fp32 stream, single-round rows only)
-template <bool ST>
-ConstructFn pick_roulette_relay(int NV) {
+template <bool ST, bool HI>
+ConstructFn pick_roulette_relay_h(int NV) {
     switch (NV) {
-    case 2: return k_construct_roulette_relay<2, ST>;
-    case 4: return k_construct_roulette_relay<4, ST>;
-    case 8: return k_construct_roulette_relay<8, ST>;
-    case 12: return k_construct_roulette_relay<12, ST>;
-    case 16: return k_construct_roulette_relay<16, ST>;
-    case 19: return k_construct_roulette_relay<19, ST>;
-    default: return k_construct_roulette_relay<20, ST>;
+    case 2: return k_construct_roulette_relay<2, ST, HI>;
+    case 4: return k_construct_roulette_relay<4, ST, HI>;
+    case 8: return k_construct_roulette_relay<8, ST, HI>;
+    case 12: return k_construct_roulette_relay<12, ST, HI>;
+    case 16: return k_construct_roulette_relay<16, ST, HI>;
+    case 19: return k_construct_roulette_relay<19, ST, HI>;
+    default: return k_construct_roulette_relay<20, ST, HI>;
     }
 }
+template <bool ST>
+ConstructFn pick_roulette_relay(int NV, bool hi) {
+    return hi ? pick_roulette_relay_h<ST, true>(NV) : pick_roulette_relay_h<ST, false>(NV);
+}
 
-template <typename WT, bool ST>
-ConstructFn pick_roulette_s(int NV, int MAXR) {
+template <typename WT, bool ST, bool HI>
+ConstructFn pick_roulette_h(int NV, int MAXR) {
     if (MAXR == 1) {
         switch (NV) {
-        case 2: return k_construct_roulette<WT, 2, 1, ST>;
-        case 4: return k_construct_roulette<WT, 4, 1, ST>;
-        case 8: return k_construct_roulette<WT, 8, 1, ST>;
-        case 12: return k_construct_roulette<WT, 12, 1, ST>;
-        case 16: return k_construct_roulette<WT, 16, 1, ST>;
-        case 19: return k_construct_roulette<WT, 19, 1, ST>;
-        default: return k_construct_roulette<WT, 20, 1, ST>;
+        case 2: return k_construct_roulette<WT, 2, 1, ST, HI>;
+        case 4: return k_construct_roulette<WT, 4, 1, ST, HI>;
+        case 8: return k_construct_roulette<WT, 8, 1, ST, HI>;
+        case 12: return k_construct_roulette<WT, 12, 1, ST, HI>;
+        case 16: return k_construct_roulette<WT, 16, 1, ST, HI>;
+        case 19: return k_construct_roulette<WT, 19, 1, ST, HI>;
+        default: return k_construct_roulette<WT, 20, 1, ST, HI>;
         }
     }
     return k_construct_roulette<WT, 20, 8, ST>;
 }
+// hi: a high-occupancy launch (>= kHiWarps warps per SM): the issue-lean step
+// (in-place scans, predicated sequential group sums), fp32 stream only
+template <typename WT, bool ST>
+ConstructFn pick_roulette_s(int NV, int MAXR, bool hi) {
+    if constexpr (sizeof(WT) == 4)
+        if (hi) return pick_roulette_h<WT, ST, true>(NV, MAXR);
+    return pick_roulette_h<WT, ST, false>(NV, MAXR);
+}
 // stream = true: the variant that also streams tours into mapped host memory
 template <typename WT>
-ConstructFn pick_roulette(int NV, int MAXR, bool stream = false) {
-    return stream ? pick_roulette_s<WT, true>(NV, MAXR) : pick_roulette_s<WT, false>(NV, MAXR);
+ConstructFn pick_roulette(int NV, int MAXR, bool stream = false, bool hi = false) {
+    return stream ? pick_roulette_s<WT, true>(NV, MAXR, hi) : pick_roulette_s<WT, false>(NV, MAXR, hi);
 }
 
 void choose_stream_layout(aco_gpu_ctx* c) {
@@ -610,8 +622,11 @@ void launch_construct(aco_gpu_ctx* c) {
         // where the GPU would idle waiting for the first launch
         auto& L = c->rlaunch[st ? 1 : 0];
         if (!L.valid) {
+        // the warps each SM will hold: >= kHiWarps -> the issue-lean step
+        constexpr int kHiWarps = 12;
+        const bool hi = (c->mloc + c->num_sms - 1) / c->num_sms >= kHiWarps;
         ConstructFn fn = c->stream_kind == ACO_STREAM_FP64 ? pick_roulette<double>(c->NV, c->MAXR, st)
-                                                           : pick_roulette<float>(c->NV, c->MAXR, st);
+                                                           : pick_roulette<float>(c->NV, c->MAXR, st, hi);
         const size_t wsz = c->stream_kind == ACO_STREAM_FP64 ? sizeof(double) : sizeof(float);
         const int ng = (c->NV + 3) / 4;
         size_t smem = 128 + static_cast<size_t>(c->PW) * wsz + smem1 +
@@ -638,7 +653,7 @@ void launch_construct(aco_gpu_ctx* c) {
         // relayed (0.82 -> 1.03 ms, tools/relay_ab.py).
         if (c->stream_kind == ACO_STREAM_FP32 && c->MAXR == 1 && E > 0 && q >= relay_min_q() &&
             q <= per_sm && q * c->num_sms >= 32 * E) {
-            ConstructFn rfn = st ? pick_roulette_relay<true>(c->NV) : pick_roulette_relay<false>(c->NV);
+            ConstructFn rfn = st ? pick_roulette_relay<true>(c->NV, hi) : pick_roulette_relay<false>(c->NV, hi);
             const size_t rsmem = smem + smem1;
             CK(cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsmem)));
             int rper_sm = 0;
@@ -676,7 +691,7 @@ void launch_construct(aco_gpu_ctx* c) {
         L.grid = grid;
         L.desc = std::string("k_construct_roulette<") +
                  (c->stream_kind == ACO_STREAM_FP64 ? "double," : "float,") +
-                 std::to_string(c->NV) + "," + std::to_string(c->MAXR) + "> grid=" +
+                 std::to_string(c->NV) + "," + std::to_string(c->MAXR) + (hi ? ",hi" : "") + "> grid=" +
                  std::to_string(grid) + " per_sm=" + std::to_string(per_sm) +
                  " smem=" + std::to_string(smem) + " row=" + std::to_string(c->PW) +
                  (st ? " streams_tours_to_host" : "") + relay_desc;

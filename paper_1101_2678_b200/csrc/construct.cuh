@@ -87,6 +87,10 @@ __host__ __device__ __forceinline__ int stream_city(int p, int C, int V, int LA 
     return r * LA * C + l * C + t * V + q;
 }
 
+#ifndef ACO_SEQ_GROUP
+#define ACO_SEQ_GROUP 1 // high-occupancy roulette: predicated sequential group sums
+#endif
+
 #ifndef ACO_FUSED_TAIL_BUILD
 #define ACO_FUSED_TAIL_BUILD 1 // 0: the kernels carry no tail (k_tour_length always runs)
 #endif
@@ -602,7 +606,7 @@ __device__ __forceinline__ void roulette_end(const ConstructParams& p, RouletteA
 
 // Steps [s0, s1) of one ant.  smem: the kernel's dynamic shared memory
 // (mbarrier, row buffer, own tabu, chunk_start, gsum).
-template <typename WT, int NV, int MAXR, bool STREAM, bool SCAN_INPLACE = false>
+template <typename WT, int NV, int MAXR, bool STREAM, bool SCAN_INPLACE = false, bool SEQG = false>
 __device__ __forceinline__ void roulette_steps(const ConstructParams& p, RouletteAnt& a, int s0, int s1,
                                                unsigned char* smem_raw, uint32_t& phase,
                                                unsigned long long& fb, unsigned long long& fb2) {
@@ -614,8 +618,13 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
     constexpr int GV = 4;                              // vectors per tree group
     constexpr int NG = (NV + GV - 1) / GV;             // groups per chunk
     constexpr int GE = GV * V;                         // cities per group
-    constexpr int D1 = ceil_log2<GE>() + ceil_log2<NG>();
     constexpr bool F32 = sizeof(WT) == 4;
+    // SEQ: high-occupancy launches (SEQG) sum each group of GE
+    // cities with predicated sequential adds (GE instructions, no masking
+    // selects) instead of masked selects + a packed tree (GE + GE/2): fewer
+    // issue slots, a longer chain (hidden by the other warps there)
+    constexpr bool SEQ = ACO_SEQ_GROUP && SEQG && F32 && MAXR == 1;
+    constexpr int D1 = (SEQ ? GE - 1 : ceil_log2<GE>()) + ceil_log2<NG>();
     // fp32 single-round rows: the group walk; otherwise the quad-scan walk
     constexpr bool kGroupWalk = F32 && MAXR == 1;
     static_assert(GE <= 32 && 32 % GE == 0, "a group's bits live in one window word");
@@ -724,6 +733,15 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
                             x[tt * 2 + 0] = v.x; x[tt * 2 + 1] = v.y;
                         }
                     }
+                    if constexpr (SEQ) {
+                        WT acc = WT(0);
+#pragma unroll
+                        for (int e = 0; e < GE; ++e) {
+                            const int ee = g * GE + e;
+                            if (ee < C && !((win[ee >> 5] >> (ee & 31)) & 1u)) acc += x[e];
+                        }
+                        gs[g] = acc;
+                    } else {
 #pragma unroll
                     for (int e = 0; e < GE; ++e) {
                         const int ee = g * GE + e;
@@ -731,6 +749,7 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
                     }
                     if constexpr (F32) gs[g] = tree_sum_packed<GE>(x);
                     else gs[g] = tree_sum<WT, GE>(x);
+                    }
                     if constexpr (MAXR > 1) gsum[(r * NG + g) * 32 + lane] = gs[g];
                 }
                 if constexpr (MAXR == 1) { // lane-local inclusive group prefixes
@@ -997,7 +1016,9 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
     a.prefetched = prefetched;
 }
 
-template <typename WT, int NV, int MAXR, bool STREAM = false>
+// HI: high-occupancy launch (the issue-lean step: in-place scans, predicated
+// sequential group sums)
+template <typename WT, int NV, int MAXR, bool STREAM = false, bool HI = false>
 __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(ConstructParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
@@ -1010,7 +1031,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
     for (int kl = blockIdx.x; kl < p.mloc; kl += gridDim.x) {
         RouletteAnt a;
         roulette_begin(p, a, kl, tabu, lane, STREAM);
-        roulette_steps<WT, NV, MAXR, STREAM>(p, a, 1, p.n, smem_raw, phase, fb, fb2);
+        roulette_steps<WT, NV, MAXR, STREAM, HI, HI>(p, a, 1, p.n, smem_raw, phase, fb, fb2);
         roulette_end(p, a, lane, STREAM);
     }
     if (lane == 0) {
@@ -1048,7 +1069,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
     return v;
 }
 
-template <int NV, bool STREAM>
+template <int NV, bool STREAM, bool HI = true>
 __global__ void __launch_bounds__(32, 16) k_construct_roulette_relay(ConstructParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
@@ -1138,7 +1159,7 @@ __global__ void __launch_bounds__(32, 16) k_construct_roulette_relay(ConstructPa
         } else {
             stage = 2;
         }
-        roulette_steps<float, NV, 1, STREAM, true>(p, ants[which], s0, s1, smem_raw, phase, fb, fb2);
+        roulette_steps<float, NV, 1, STREAM, true, HI>(p, ants[which], s0, s1, smem_raw, phase, fb, fb2);
         if (which == 0) s = s1;
     }
     roulette_end(p, ants[0], lane, STREAM);
@@ -1217,6 +1238,9 @@ __global__ void __launch_bounds__(32) k_construct_roulette_exact(ConstructParams
 #ifndef ACO_NN_MINB
 #define ACO_NN_MINB 28 // resident warps per SM the register budget must allow
 #endif
+#ifndef ACO_NN_LA
+#define ACO_NN_LA 0 // SPEC launches: lists of the first K (1, 2) unvisited members loaded ahead
+#endif
 // SPEC: the crossing candidate's list is requested before its certification
 // (for latency-bound launches; that variant is held to 64 registers)
 // FAST32: nn <= 32 with the row-scaled fp32 list weights (the fast path)
@@ -1257,6 +1281,10 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
         int jg = -1;
         int jspec = -1;
         float wspec = 0.f;
+#if ACO_NN_LA > 0
+        int la_c0 = -1, la_j0 = -1, la_c1 = -1, la_j1 = -1;
+        float la_w0 = 0.f, la_w1 = 0.f;
+#endif
         // kHold (full-occupancy launches): the open 32-entry chunk of the
         // tour (and of the list positions) is held in the lanes — lane
         // (s & 31) holds tour[s] / qpos[s-1] — and stored coalesced when the
@@ -1309,6 +1337,26 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                     w = un ? wpre : 0.f;
                 }
                 const unsigned unb = __ballot_sync(kFull, un);
+#if ACO_NN_LA > 0
+                // lookahead: the lists of the first ACO_NN_LA unvisited
+                // members (the likely next cities) are loaded now, a scan
+                // earlier than the chosen one's could be
+                if (SPEC && unb && step + 1 < n) {
+                    la_c0 = __shfl_sync(kFull, j, __ffs(unb) - 1);
+                    if (lane < nn) {
+                        la_j0 = p.nn_lists[static_cast<size_t>(la_c0) * nn + lane];
+                        la_w0 = p.choice_nn32[static_cast<size_t>(la_c0) * nn + lane];
+                    }
+#if ACO_NN_LA > 1
+                    const unsigned unb2 = unb & (unb - 1u);
+                    la_c1 = unb2 ? __shfl_sync(kFull, j, __ffs(unb2) - 1) : -1;
+                    if (lane < nn && la_c1 >= 0) {
+                        la_j1 = p.nn_lists[static_cast<size_t>(la_c1) * nn + lane];
+                        la_w1 = p.choice_nn32[static_cast<size_t>(la_c1) * nn + lane];
+                    }
+#endif
+                }
+#endif
                 if (!unb) {
                     exhausted = true;
                 } else {
@@ -1325,7 +1373,14 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                         const float PJ = __shfl_sync(kFull, P, J);
                         const float EJ = __shfl_sync(kFull, E, J);
                         const int Jc = __shfl_sync(kFull, j, J);
-                        if (SPEC && lane < nn && step + 1 < n) {
+                        if (SPEC && lane < nn && step + 1 < n
+#if ACO_NN_LA > 0
+                            && Jc != la_c0
+#endif
+#if ACO_NN_LA > 1
+                            && Jc != la_c1
+#endif
+                            ) {
                             // the candidate's list, requested before its
                             // certification (which almost always passes)
                             jg = Jc;
@@ -1551,6 +1606,16 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                 if (SPEC && next == jg) { // the speculated list is the one
                     jpre = jspec;
                     wpre = wspec;
+#if ACO_NN_LA > 0
+                } else if (SPEC && next == la_c0) {
+                    jpre = la_j0;
+                    wpre = la_w0;
+#endif
+#if ACO_NN_LA > 1
+                } else if (SPEC && next == la_c1) {
+                    jpre = la_j1;
+                    wpre = la_w1;
+#endif
                 } else if (lane < nn) {
                     jpre = p.nn_lists[static_cast<size_t>(next) * nn + lane];
                     wpre = p.choice_nn32[static_cast<size_t>(next) * nn + lane];
