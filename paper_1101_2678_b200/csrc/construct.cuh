@@ -1238,9 +1238,6 @@ __global__ void __launch_bounds__(32) k_construct_roulette_exact(ConstructParams
 #ifndef ACO_NN_MINB
 #define ACO_NN_MINB 28 // resident warps per SM the register budget must allow
 #endif
-#ifndef ACO_NN_LA
-#define ACO_NN_LA 0 // SPEC launches: lists of the first K (1, 2) unvisited members loaded ahead
-#endif
 // SPEC: the crossing candidate's list is requested before its certification
 // (for latency-bound launches; that variant is held to 64 registers)
 // FAST32: nn <= 32 with the row-scaled fp32 list weights (the fast path)
@@ -1281,10 +1278,6 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
         int jg = -1;
         int jspec = -1;
         float wspec = 0.f;
-#if ACO_NN_LA > 0
-        int la_c0 = -1, la_j0 = -1, la_c1 = -1, la_j1 = -1;
-        float la_w0 = 0.f, la_w1 = 0.f;
-#endif
         // kHold (full-occupancy launches): the open 32-entry chunk of the
         // tour (and of the list positions) is held in the lanes — lane
         // (s & 31) holds tour[s] / qpos[s-1] — and stored coalesced when the
@@ -1337,26 +1330,6 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                     w = un ? wpre : 0.f;
                 }
                 const unsigned unb = __ballot_sync(kFull, un);
-#if ACO_NN_LA > 0
-                // lookahead: the lists of the first ACO_NN_LA unvisited
-                // members (the likely next cities) are loaded now, a scan
-                // earlier than the chosen one's could be
-                if (SPEC && unb && step + 1 < n) {
-                    la_c0 = __shfl_sync(kFull, j, __ffs(unb) - 1);
-                    if (lane < nn) {
-                        la_j0 = p.nn_lists[static_cast<size_t>(la_c0) * nn + lane];
-                        la_w0 = p.choice_nn32[static_cast<size_t>(la_c0) * nn + lane];
-                    }
-#if ACO_NN_LA > 1
-                    const unsigned unb2 = unb & (unb - 1u);
-                    la_c1 = unb2 ? __shfl_sync(kFull, j, __ffs(unb2) - 1) : -1;
-                    if (lane < nn && la_c1 >= 0) {
-                        la_j1 = p.nn_lists[static_cast<size_t>(la_c1) * nn + lane];
-                        la_w1 = p.choice_nn32[static_cast<size_t>(la_c1) * nn + lane];
-                    }
-#endif
-                }
-#endif
                 if (!unb) {
                     exhausted = true;
                 } else {
@@ -1373,14 +1346,7 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                         const float PJ = __shfl_sync(kFull, P, J);
                         const float EJ = __shfl_sync(kFull, E, J);
                         const int Jc = __shfl_sync(kFull, j, J);
-                        if (SPEC && lane < nn && step + 1 < n
-#if ACO_NN_LA > 0
-                            && Jc != la_c0
-#endif
-#if ACO_NN_LA > 1
-                            && Jc != la_c1
-#endif
-                            ) {
+                        if (SPEC && lane < nn && step + 1 < n) {
                             // the candidate's list, requested before its
                             // certification (which almost always passes)
                             jg = Jc;
@@ -1606,16 +1572,6 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                 if (SPEC && next == jg) { // the speculated list is the one
                     jpre = jspec;
                     wpre = wspec;
-#if ACO_NN_LA > 0
-                } else if (SPEC && next == la_c0) {
-                    jpre = la_j0;
-                    wpre = la_w0;
-#endif
-#if ACO_NN_LA > 1
-                } else if (SPEC && next == la_c1) {
-                    jpre = la_j1;
-                    wpre = la_w1;
-#endif
                 } else if (lane < nn) {
                     jpre = p.nn_lists[static_cast<size_t>(next) * nn + lane];
                     wpre = p.choice_nn32[static_cast<size_t>(next) * nn + lane];
