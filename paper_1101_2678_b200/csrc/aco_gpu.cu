@@ -180,7 +180,7 @@ struct aco_gpu_ctx {
     int32_t* d_scale = nullptr;
     int32_t* d_nn = nullptr;
     double* d_choice_nn = nullptr; // n x nn
-    float* d_choice_nn32 = nullptr; // n x nn, row-scaled fp32 (nn <= 32)
+    int2* d_choice_nn32 = nullptr;  // n x nn {id, row-scaled fp32 weight bits} (nn <= 32)
     int32_t* d_nn_scale = nullptr;  // n
     int32_t* d_topk = nullptr;     // n x kTopK argmax cache (nn selection)
     long long last_fb[2] = {0, 0}; // last construction: exact/full-scan, argmax fallbacks
@@ -1506,7 +1506,7 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
                           cudaMemcpyHostToDevice));
             CK(cudaMalloc(&c->d_choice_nn, nn_host.size() * sizeof(double)));
             if (c->cfg.nn <= 32) {
-                CK(cudaMalloc(&c->d_choice_nn32, nn_host.size() * sizeof(float)));
+                CK(cudaMalloc(&c->d_choice_nn32, nn_host.size() * sizeof(int2)));
                 CK(cudaMalloc(&c->d_nn_scale, n * sizeof(int32_t)));
             }
             const char* tke = std::getenv("ACO_NN_TOPK"); // "0" disables the argmax cache

@@ -100,7 +100,7 @@ struct ConstructParams {
     const double* w64;       // natural fp64 choice, row pitch P64 (exact walk, nn)
     const int32_t* nn_lists; // n x nn (nn selection)
     const double* choice_nn; // n x nn weights of the nn lists (nn selection)
-    const float* choice_nn32; // n x nn, row-scaled fp32 copy (nn <= 32) or null
+    const int2* choice_nn32;  // n x nn {city id, row-scaled fp32 weight bits} (nn <= 32) or null
     int32_t* tours;          // mloc x (n+1)
     unsigned long long* fallbacks;
     unsigned long long* argmax_fallbacks;
@@ -1285,8 +1285,11 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
         constexpr bool kHold = !SPEC;
         int held_t = 0, held_q = 0;
         if (fast32 && lane < nn) {
-            jpre = p.nn_lists[static_cast<size_t>(start) * nn + lane];
-            wpre = p.choice_nn32[static_cast<size_t>(start) * nn + lane];
+            {
+                const int2 rec = p.choice_nn32[static_cast<unsigned>(start * nn + lane)];
+                jpre = rec.x;
+                wpre = __int_as_float(rec.y);
+            }
         }
         for (int step = 1; step < n; ++step) {
             const double* __restrict__ row = p.w64 + static_cast<size_t>(cur) * p.P64;
@@ -1350,8 +1353,11 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                             // the candidate's list, requested before its
                             // certification (which almost always passes)
                             jg = Jc;
-                            jspec = p.nn_lists[static_cast<size_t>(Jc) * nn + lane];
-                            wspec = p.choice_nn32[static_cast<size_t>(Jc) * nn + lane];
+                            {
+                                const int2 rec = p.choice_nn32[static_cast<unsigned>(Jc * nn + lane)];
+                                jspec = rec.x;
+                                wspec = __int_as_float(rec.y);
+                            }
                         }
                         // thresholds in fp32, every operation rounded
                         // outward: A32 >= u*T + Mt + 2*abs, B32 <= u*T - Mt -
@@ -1573,8 +1579,11 @@ __global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(Co
                     jpre = jspec;
                     wpre = wspec;
                 } else if (lane < nn) {
-                    jpre = p.nn_lists[static_cast<size_t>(next) * nn + lane];
-                    wpre = p.choice_nn32[static_cast<size_t>(next) * nn + lane];
+                    {
+                        const int2 rec = p.choice_nn32[static_cast<unsigned>(next * nn + lane)];
+                        jpre = rec.x;
+                        wpre = __int_as_float(rec.y);
+                    }
                 }
             }
             jg = -1;

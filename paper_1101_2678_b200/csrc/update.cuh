@@ -481,7 +481,7 @@ struct RowParams {
     const double* inv;       // [shard][S]
     const int32_t* nn_lists; // n x nn (nn selection) or null
     double* choice_nn;       // n x nn: choice64[i][nn_lists[i][q]] (nn selection)
-    float* choice_nn32;      // n x nn: the same scaled by 2^nn_scale[i] (row max -> [2^kScaleExp, 2^(kScaleExp+1))), fp32
+    int2* choice_nn32;       // n x nn records {city id, fp32 bits of the weight scaled by 2^nn_scale[i]} (row max -> [2^kScaleExp, 2^(kScaleExp+1))): one 8-byte load per member in the nn fast path
     int32_t* nn_scale;       // n
     int nn;
     int n, P64, PW, C, V, LA;
@@ -553,7 +553,9 @@ __device__ __forceinline__ void write_nn_row(const RowParams& p, const double* s
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, off));
         const int sc = mx > 0.0 ? kScaleExp - ilogb(mx) : 0;
-        if (lane < p.nn) p.choice_nn32[base + lane] = __double2float_rn(scalbn(w, sc));
+        if (lane < p.nn)
+            p.choice_nn32[base + lane] =
+                make_int2(p.nn_lists[base + lane], __float_as_int(__double2float_rn(scalbn(w, sc))));
         if (lane == 0) p.nn_scale[i] = sc;
     }
 }
