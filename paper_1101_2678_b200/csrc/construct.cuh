@@ -651,6 +651,8 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
     const double lo_f = 1.0 - e_rel;
     const float lo32 = __double2float_rd(lo_f); // <= lo_f
     const float e32 = __double2float_ru(e_rel); // >= e_rel
+    const float ce32 = __double2float_ru(e_rel + 4.0 * ulp_at); // >= the Mt coefficient
+    const float absq32 = __double2float_ru(abs_q);              // n * 2^-149 (exact)
 
     const int kl = a.kl;
     const uint32_t kg = a.kg;
@@ -667,8 +669,12 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
     // Draw 0 of steps b..b+31 (b = 1 mod 32): lane i holds step b + i
     // (rng.hpp:74-80); a run starting inside a batch draws it first.
     double ubatch = 0.0;
-    if (((s0 - 1) & 31) != 0)
+    float ub_dn = 0.f, ub_up = 0.f; // kGroupWalk: the draw rounded down / up
+    if (((s0 - 1) & 31) != 0) {
         ubatch = philox_uniform(p.seed, p.iteration, kg, static_cast<uint32_t>(((s0 - 1) & ~31) + 1 + lane), 0);
+        ub_dn = __double2float_rd(ubatch);
+        ub_up = __double2float_ru(ubatch);
+    }
 #if ACO_TIMING
     unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long tk = clock64();
@@ -684,11 +690,26 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
             tma_row(buf, wbase + static_cast<size_t>(cur) * p.PW, row_bytes, bar);
         }
         // Draw 0 of steps step..step+31: lane i holds step + i (rng.hpp:74-80).
-        if (((step - 1) & 31) == 0)
+        if (((step - 1) & 31) == 0) {
             ubatch = philox_uniform(p.seed, p.iteration, kg,
                                     static_cast<uint32_t>(step + lane), 0);
-        const double u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
-        const float u32 = __double2float_rn(u);
+            if constexpr (kGroupWalk) {
+                ub_dn = __double2float_rd(ubatch);
+                ub_up = __double2float_ru(ubatch);
+            }
+        }
+        // the group walk brackets u by the float pair (u_dn <= u <= u_up):
+        // candidate and certification thresholds in fp32, no conversions;
+        // the fp64 draw is shuffled only when a fallback tier runs
+        double u = 0.0;
+        float u32 = 0.f, u_dn = 0.f, u_up = 0.f;
+        if constexpr (kGroupWalk) {
+            u_dn = __shfl_sync(kFull, ub_dn, (step - 1) & 31);
+            u_up = __shfl_sync(kFull, ub_up, (step - 1) & 31);
+        } else {
+            u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
+            u32 = __double2float_rn(u);
+        }
         __syncwarp();
         mbar_wait(bar, phase);
         phase ^= 1u;
@@ -782,14 +803,26 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
         // the top of the step), keeping the double product and its two
         // conversions off the scan -> ballot chain.
         AT t;
-        if constexpr (F32) t = __fmul_rn(u32, T);
+        if constexpr (kGroupWalk) t = __fmul_rn(u_dn, T);
+        else if constexpr (F32) t = __fmul_rn(u32, T);
         else t = static_cast<AT>(tdd);
         // certification thresholds (T, u only): |t_ref - t| <= Mt
         const double Thi = Td * (1.0 + 0x1.0p-16) + abs_q;
         const double Mt = (e_rel + 4.0 * ulp_at) * (u * Thi) + abs_q; // + rounding of t to AT
         const double A = tdd + Mt + 2.0 * abs_q; // need Pj * (1 - e) > A
         const double B = tdd - Mt - 2.0 * abs_q; // need Pprev + e * Pj < B
-        bool ok = (T > AT(0)) && (Td < 1e300);
+        // the group walk's fp32 form, every operation rounded outward:
+        // A32 >= u*T + Mt + 2*abs >= A's real value, B32 <= u*T - Mt - 2*abs
+        float A32 = 0.f, B32 = 0.f;
+        if constexpr (kGroupWalk) {
+            const float Thi32 = __fadd_ru(__fmul_ru(T, 1.0f + 0x1.0p-16f), absq32);
+            const float Mt32 = __fadd_ru(__fmul_ru(ce32, __fmul_ru(u_up, Thi32)), absq32);
+            A32 = __fadd_ru(__fadd_ru(__fmul_ru(u_up, T), Mt32), 2.0f * absq32);
+            B32 = __fsub_rd(__fsub_rd(__fmul_rd(u_dn, T), Mt32), 2.0f * absq32);
+        }
+        bool ok;
+        if constexpr (kGroupWalk) ok = (T > AT(0)) && (T <= 0x1.fffffep127f);
+        else ok = (T > AT(0)) && (Td < 1e300);
         int next = -1;
         if (ok) {
             AT base = AT(0), my = AT(0);
@@ -870,8 +903,6 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
                         // (implies the fp64 form): Pj*lo_f >= rd(Pj*lo32) >
                         // A32 >= A and Pprev + e*Pj <= ru(Pprev + ru(e32*Pj))
                         // < B32 <= B, with lo32 <= lo_f, e32 >= e_rel.
-                        const float A32 = __double2float_ru(A);
-                        const float B32 = __double2float_rd(B);
                         const int Jc = c0 + E;
                         J = mine ? Jc : -1;
                         cert = mine && (__fmul_rd(Pj32, lo32) > A32) &&
@@ -966,6 +997,7 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
         }
         TICK(3);
         if (!ok) { // middle tier: fp64 sums over the fp32 row still in smem
+            if constexpr (kGroupWalk) u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
             const int j2 = certify_fp64<WT, NV, MAXR>(buf, tabu, n, p.R, u, lane);
             if (j2 >= 0) {
                 ok = true;
