@@ -725,7 +725,7 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
         for (int r = 0; r < MAXR; ++r) {
             incl[r] = AT(0);
             rtot[r] = AT(0);
-            if (r < p.R) {
+            if (MAXR == 1 || r < p.R) { // single-round layouts have R == 1
                 const int cbase = r * 32 * C + lane * C;
                 const int w0 = cbase >> 5, sh = cbase & 31;
                 uint32_t win[NWIN];
@@ -829,7 +829,7 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
             int rs = -1;
 #pragma unroll
             for (int r = 0; r < MAXR; ++r) {
-                if (r < p.R && rs < 0) {
+                if ((MAXR == 1 || r < p.R) && rs < 0) {
                     if (base + rtot[r] > t) {
                         rs = r;
                         my = incl[r];
