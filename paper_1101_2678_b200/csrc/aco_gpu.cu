@@ -574,7 +574,7 @@ ConstructParams make_cp(aco_gpu_ctx* c) {
 int relay_min_q() {
     static const int q = [] {
         const char* e = std::getenv("ACO_RELAY");
-        return e ? (std::atoi(e) <= 0 ? 1 << 30 : std::atoi(e)) : 4;
+        return e ? (std::atoi(e) <= 0 ? 1 << 30 : std::atoi(e)) : 8;
     }();
     return q;
 }
@@ -651,8 +651,12 @@ void launch_construct(aco_gpu_ctx* c) {
         // Only when the leftovers are few (W >= 32 E: every relay warp carries
         // at most ~1/32 of an ant more); pr1002 (E = 114 of 888) runs slower
         // relayed (0.82 -> 1.03 ms, tools/relay_ab.py).
+        // The leftover warp only hurts where it creates a new busiest SM
+        // sub-partition (a one-warp CTA lands on one of 4 schedulers): q a
+        // multiple of 4.  Measured (profiles/relay_q_ab_r02.txt): relay wins
+        // at q = 8 (-4.6%) and 16 (-8%), loses at q = 4 (+2.7%) and 5-7 (+6-7%).
         if (c->stream_kind == ACO_STREAM_FP32 && c->MAXR == 1 && E > 0 && q >= relay_min_q() &&
-            q <= per_sm && q * c->num_sms >= 32 * E) {
+            q % 4 == 0 && q <= per_sm && q * c->num_sms >= 32 * E) {
             ConstructFn rfn = st ? pick_roulette_relay<true>(c->NV, hi) : pick_roulette_relay<false>(c->NV, hi);
             const size_t rsmem = smem + smem1;
             CK(cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsmem)));
