@@ -153,6 +153,7 @@ struct aco_gpu_ctx {
     int rank = 0, world = 1, ant_begin = 0, ant_end = 0, mloc = 0, S = 0;
     int P64 = 0, PW = 0, NV = 0, V = 4, C = 0, R = 1, MAXR = 1, tabu_words = 0;
     int LA = 32;          // lanes sharing a streamed row
+    bool nat = false;     // streamed rows in the natural layout (RowLayout; plain launches, odd NV)
     bool exact_only = false; // k_construct_roulette_exact (rows too long to stream)
     int32_t* host_tours = nullptr; // this construction's streamed host tour buffer (device view)
     double tau0 = 0.0;
@@ -324,7 +325,7 @@ ConstructFn pick_roulette_relay(int NV, bool hi) {
 }
 
 template <typename WT, bool ST, bool HI>
-ConstructFn pick_roulette_h(int NV, int MAXR) {
+ConstructFn pick_roulette_h(int NV, int MAXR, bool nat) {
     if (MAXR == 1) {
         switch (NV) {
         case 2: return k_construct_roulette<WT, 2, 1, ST, HI>;
@@ -332,24 +333,38 @@ ConstructFn pick_roulette_h(int NV, int MAXR) {
         case 8: return k_construct_roulette<WT, 8, 1, ST, HI>;
         case 12: return k_construct_roulette<WT, 12, 1, ST, HI>;
         case 16: return k_construct_roulette<WT, 16, 1, ST, HI>;
-        case 19: return k_construct_roulette<WT, 19, 1, ST, HI>;
+        case 19:
+            if constexpr (sizeof(WT) == 4)
+                if (nat) return k_construct_roulette<WT, 19, 1, ST, HI, true>;
+            return k_construct_roulette<WT, 19, 1, ST, HI>;
         default: return k_construct_roulette<WT, 20, 1, ST, HI>;
         }
     }
     return k_construct_roulette<WT, 20, 8, ST>;
 }
 // hi: a high-occupancy launch (>= kHiWarps warps per SM): the issue-lean step
-// (in-place scans, predicated sequential group sums), fp32 stream only
+// (in-place scans, predicated sequential group sums), fp32 stream only;
+// nat: the natural row layout (odd NV)
 template <typename WT, bool ST>
-ConstructFn pick_roulette_s(int NV, int MAXR, bool hi) {
+ConstructFn pick_roulette_s(int NV, int MAXR, bool hi, bool nat) {
     if constexpr (sizeof(WT) == 4)
-        if (hi) return pick_roulette_h<WT, ST, true>(NV, MAXR);
-    return pick_roulette_h<WT, ST, false>(NV, MAXR);
+        if (hi) return pick_roulette_h<WT, ST, true>(NV, MAXR, nat);
+    return pick_roulette_h<WT, ST, false>(NV, MAXR, nat);
 }
 // stream = true: the variant that also streams tours into mapped host memory
 template <typename WT>
-ConstructFn pick_roulette(int NV, int MAXR, bool stream = false, bool hi = false) {
-    return stream ? pick_roulette_s<WT, true>(NV, MAXR, hi) : pick_roulette_s<WT, false>(NV, MAXR, hi);
+ConstructFn pick_roulette(int NV, int MAXR, bool stream = false, bool hi = false, bool nat = false) {
+    return stream ? pick_roulette_s<WT, true>(NV, MAXR, hi, nat) : pick_roulette_s<WT, false>(NV, MAXR, hi, nat);
+}
+
+int relay_min_q();
+// Will the roulette construction use the relay launch (see the launch
+// below)?  Decides the streamed-row layout before the first launch; the
+// launch never relays a natural-layout context.
+bool relay_predicted(const aco_gpu_ctx* c) {
+    if (c->num_sms <= 0 || c->mloc <= 0) return false;
+    const int q = c->mloc / c->num_sms, E = c->mloc - q * c->num_sms;
+    return E > 0 && q >= relay_min_q() && q % 4 == 0 && q * c->num_sms >= 32 * E;
 }
 
 void choose_stream_layout(aco_gpu_ctx* c) {
@@ -383,7 +398,10 @@ void choose_stream_layout(aco_gpu_ctx* c) {
         return;
     }
     c->C = c->NV * c->V;
-    c->PW = c->R * kLP * c->C;        // physical row length (with pad slots)
+    // physical row length: the natural layout (odd NV) when the launch will
+    // be the plain one-warp-per-ant kernel, else with pad slots
+    c->nat = (c->NV & 1) && c->MAXR == 1 && c->stream_kind == ACO_STREAM_FP32 && !relay_predicted(c);
+    c->PW = c->R * (c->nat ? 32 : kLP) * c->C;
     c->tabu_words = c->R * c->C + 4;  // covers R*32*C cities; even, keeps the fp64 area 8-aligned
 }
 
@@ -427,6 +445,7 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
     rp.C = c->C;
     rp.V = c->V;
     rp.LA = c->LA;
+    rp.nat = c->nat ? 1 : 0;
     rp.shards = c->world;
     rp.S = c->S;
     rp.m = !c->sharded ? c->mloc : c->m; // a local ant range is one shard of mloc ants
@@ -626,7 +645,7 @@ void launch_construct(aco_gpu_ctx* c) {
         constexpr int kHiWarps = 12;
         const bool hi = (c->mloc + c->num_sms - 1) / c->num_sms >= kHiWarps;
         ConstructFn fn = c->stream_kind == ACO_STREAM_FP64 ? pick_roulette<double>(c->NV, c->MAXR, st)
-                                                           : pick_roulette<float>(c->NV, c->MAXR, st, hi);
+                                                           : pick_roulette<float>(c->NV, c->MAXR, st, hi, c->nat);
         const size_t wsz = c->stream_kind == ACO_STREAM_FP64 ? sizeof(double) : sizeof(float);
         const int ng = (c->NV + 3) / 4;
         size_t smem = 128 + static_cast<size_t>(c->PW) * wsz + smem1 +
@@ -656,7 +675,7 @@ void launch_construct(aco_gpu_ctx* c) {
         // multiple of 4.  Measured (profiles/relay_q_ab_r02.txt): relay wins
         // at q = 8 (-4.6%) and 16 (-8%), loses at q = 4 (+2.7%) and 5-7 (+6-7%).
         if (c->stream_kind == ACO_STREAM_FP32 && c->MAXR == 1 && E > 0 && q >= relay_min_q() &&
-            q % 4 == 0 && q <= per_sm && q * c->num_sms >= 32 * E) {
+            q % 4 == 0 && q <= per_sm && q * c->num_sms >= 32 * E && !c->nat) {
             ConstructFn rfn = st ? pick_roulette_relay<true>(c->NV, hi) : pick_roulette_relay<false>(c->NV, hi);
             const size_t rsmem = smem + smem1;
             CK(cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsmem)));
@@ -695,7 +714,7 @@ void launch_construct(aco_gpu_ctx* c) {
         L.grid = grid;
         L.desc = std::string("k_construct_roulette<") +
                  (c->stream_kind == ACO_STREAM_FP64 ? "double," : "float,") +
-                 std::to_string(c->NV) + "," + std::to_string(c->MAXR) + (hi ? ",hi" : "") + "> grid=" +
+                 std::to_string(c->NV) + "," + std::to_string(c->MAXR) + (hi ? ",hi" : "") + (c->nat ? ",nat" : "") + "> grid=" +
                  std::to_string(grid) + " per_sm=" + std::to_string(per_sm) +
                  " smem=" + std::to_string(smem) + " row=" + std::to_string(c->PW) +
                  (st ? " streams_tours_to_host" : "") + relay_desc;
@@ -1921,7 +1940,7 @@ aco_status aco_gpu_get_choice32(aco_gpu_ctx* c, float* choice, int32_t* scale_ex
         for (int i = 0; i < c->n; ++i)
             for (int j = 0; j < c->n; ++j)
                 choice[static_cast<size_t>(i) * c->n + j] =
-                    raw[static_cast<size_t>(i) * c->PW + stream_pos(j, c->C, 4, c->LA)];
+                    raw[static_cast<size_t>(i) * c->PW + stream_pos(j, c->C, 4, c->LA, c->nat)];
     });
 }
 

@@ -69,7 +69,24 @@ template <> struct VecOf<double> {
 constexpr int kPad = ACO_PAD_SLOT;
 constexpr int kLP = 32 + kPad; // (LA + pad) for LA = 32
 
-__host__ __device__ __forceinline__ int stream_pos(int c, int C, int V, int LA = 32) {
+// Odd NV (vectors per lane chunk) may use the NATURAL layout instead (the
+// context's `nat`: plain launches only — the relay launch measured slower
+// with it, profiles/nat_layout_ab_r02.txt): city c at
+// position c, lane l's vector t at slot l*NV + t.  Reading vector t of every
+// lane strides the lanes NV (odd) slots apart, which spreads 32 lanes evenly
+// over the 8 bank groups, and a lane's consecutive vectors sit in consecutive
+// slots — conflict-free for both access patterns without a pad slot (pr2392:
+// NV = 19, rows of 2432 floats instead of 2508).
+template <int NV, bool NAT>
+struct RowLayout {
+    static constexpr bool nat = NAT && (NV & 1) != 0;
+    static constexpr int lstr = nat ? NV : 1;               // vector stride between lanes
+    static constexpr int tstr = nat ? 1 : kLP;              // between a lane's vectors
+    static constexpr int round_vecs = nat ? 32 * NV : kLP * NV; // vectors per round
+};
+
+__host__ __device__ __forceinline__ int stream_pos(int c, int C, int V, int LA = 32, bool nat = false) {
+    if (nat && ((C / V) & 1)) return c; // natural layout (odd NV)
     const int RC = LA * C, LP = LA + kPad;
     const int r = c / RC, rem = c - r * RC;
     const int l = rem / C, e = rem - l * C;
@@ -78,7 +95,8 @@ __host__ __device__ __forceinline__ int stream_pos(int c, int C, int V, int LA =
 }
 
 // Inverse of stream_pos; returns INT_MAX for pad slots.
-__host__ __device__ __forceinline__ int stream_city(int p, int C, int V, int LA = 32) {
+__host__ __device__ __forceinline__ int stream_city(int p, int C, int V, int LA = 32, bool nat = false) {
+    if (nat && ((C / V) & 1)) return p; // natural layout (odd NV)
     const int LP = LA + kPad, RS = LP * C;
     const int r = p / RS, rem = p - r * RS;
     const int t = rem / (LP * V), rem2 = rem - t * LP * V;
@@ -449,7 +467,7 @@ __device__ __forceinline__ int start_city(const ConstructParams& p, uint32_t kg)
 // is the fp32 quantisation of the weights (2^-24 relative + 2^-150 absolute per
 // city), so the uncertainty band is ~15x narrower than the fp32 pass's.
 // Returns the certified city or -1.
-template <typename WT, int NV, int MAXR>
+template <typename WT, int NV, int MAXR, bool NAT = false>
 __device__ __noinline__ int certify_fp64(const WT* buf, const uint32_t* tabu, int n, int R,
                                           double u, int lane) {
     using VT = typename VecOf<WT>::T;
@@ -474,11 +492,12 @@ __device__ __noinline__ int certify_fp64(const WT* buf, const uint32_t* tabu, in
             uint32_t win[NWIN];
 #pragma unroll
             for (int i = 0; i < NWIN; ++i) win[i] = __funnelshift_r(tabu[w0 + i], tabu[w0 + i + 1], sh);
-            const VT* rv = reinterpret_cast<const VT*>(buf + r * kLP * C) + lane;
+            const VT* rv = reinterpret_cast<const VT*>(buf + r * RowLayout<NV, NAT>::round_vecs * V) +
+                           lane * RowLayout<NV, NAT>::lstr;
             double acc = 0.0;
 #pragma unroll
             for (int tv = 0; tv < NV; ++tv) {
-                const VT v = rv[tv * kLP];
+                const VT v = rv[tv * RowLayout<NV, NAT>::tstr];
                 WT xs[V];
                 if constexpr (F32) { xs[0] = v.x; xs[1] = v.y; xs[2] = v.z; xs[3] = v.w; }
                 else { xs[0] = v.x; xs[1] = v.y; }
@@ -525,11 +544,11 @@ __device__ __noinline__ int certify_fp64(const WT* buf, const uint32_t* tabu, in
     if (lane == L) {
         double acc = base + (my - mys);
         const int cbase = rs * 32 * C + L * C;
-        const WT* chunk = buf + rs * kLP * C;
+        const WT* chunk = buf + rs * RowLayout<NV, NAT>::round_vecs * V;
         for (int e = 0; e < C; ++e) {
             const int c = cbase + e;
             if (tabu_test(tabu, c)) continue;
-            const double x = static_cast<double>(chunk[((e / V) * kLP + L) * V + (e % V)]);
+            const double x = static_cast<double>(chunk[((e / V) * RowLayout<NV, NAT>::tstr + L * RowLayout<NV, NAT>::lstr) * V + (e % V)]);
             const double na = acc + x;
             if (x > 0.0 && na > t) {
                 const double Thi = T * (1.0 + 0x1.0p-16) + abs_q;
@@ -606,7 +625,8 @@ __device__ __forceinline__ void roulette_end(const ConstructParams& p, RouletteA
 
 // Steps [s0, s1) of one ant.  smem: the kernel's dynamic shared memory
 // (mbarrier, row buffer, own tabu, chunk_start, gsum).
-template <typename WT, int NV, int MAXR, bool STREAM, bool SCAN_INPLACE = false, bool SEQG = false>
+template <typename WT, int NV, int MAXR, bool STREAM, bool SCAN_INPLACE = false, bool SEQG = false,
+          bool NAT = false>
 __device__ __forceinline__ void roulette_steps(const ConstructParams& p, RouletteAnt& a, int s0, int s1,
                                                unsigned char* smem_raw, uint32_t& phase,
                                                unsigned long long& fb, unsigned long long& fb2) {
@@ -619,6 +639,7 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
     constexpr int NG = (NV + GV - 1) / GV;             // groups per chunk
     constexpr int GE = GV * V;                         // cities per group
     constexpr bool F32 = sizeof(WT) == 4;
+    using RL = RowLayout<NV, NAT>;
     // SEQ: high-occupancy launches (SEQG) sum each group of GE
     // cities with predicated sequential adds (GE instructions, no masking
     // selects) instead of masked selects + a packed tree (GE + GE/2): fewer
@@ -732,7 +753,7 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
 #pragma unroll
                 for (int i = 0; i < NWIN; ++i)
                     win[i] = __funnelshift_r(tabu[w0 + i], tabu[w0 + i + 1], sh);
-                const VT* rv = reinterpret_cast<const VT*>(rowsrc + r * kLP * C) + lane;
+                const VT* rv = reinterpret_cast<const VT*>(rowsrc + r * RL::round_vecs * V) + lane * RL::lstr;
                 WT gs[NG];
 #pragma unroll
                 for (int g = 0; g < NG; ++g) {
@@ -742,7 +763,7 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
                         const int tv = g * GV + tt;
                         VT v;
                         if (tv < NV) {
-                            v = rv[tv * kLP];
+                            v = rv[tv * RL::tstr];
                         } else {
                             if constexpr (F32) v = make_float4(0.f, 0.f, 0.f, 0.f);
                             else v = make_double2(0.0, 0.0);
@@ -874,7 +895,7 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
                         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                         uint32_t bits4 = 0xFu;
                         if (tv < NV) {
-                            v = reinterpret_cast<const float4*>(buf)[tv * kLP + L];
+                            v = reinterpret_cast<const float4*>(buf)[tv * RL::tstr + L * RL::lstr];
                             bits4 = __funnelshift_r(tabu[c0 >> 5], tabu[(c0 >> 5) + 1], c0 & 31);
                         }
                         AT x0 = (bits4 & 1u) ? AT(0) : v.x;
@@ -927,14 +948,14 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
                     AT xv[4];
                     if constexpr (F32) {
                         const float4* qp = reinterpret_cast<const float4*>(
-                            rowsrc + rs * kLP * C + (ql * kLP + L) * 4);
+                            rowsrc + rs * RL::round_vecs * V + (ql * RL::tstr + L * RL::lstr) * 4);
                         const float4 v = *qp;
                         xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
                     } else {
                         const double2 v0 = *reinterpret_cast<const double2*>(
-                            buf + rs * kLP * C + ((2 * ql) * kLP + L) * 2);
+                            buf + rs * RL::round_vecs * V + ((2 * ql) * RL::tstr + L * RL::lstr) * 2);
                         const double2 v1 = *reinterpret_cast<const double2*>(
-                            buf + rs * kLP * C + ((2 * ql + 1) * kLP + L) * 2);
+                            buf + rs * RL::round_vecs * V + ((2 * ql + 1) * RL::tstr + L * RL::lstr) * 2);
                         xv[0] = v0.x; xv[1] = v0.y; xv[2] = v1.x; xv[3] = v1.y;
                     }
                     {
@@ -998,7 +1019,7 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
         TICK(3);
         if (!ok) { // middle tier: fp64 sums over the fp32 row still in smem
             if constexpr (kGroupWalk) u = __shfl_sync(kFull, ubatch, (step - 1) & 31);
-            const int j2 = certify_fp64<WT, NV, MAXR>(buf, tabu, n, p.R, u, lane);
+            const int j2 = certify_fp64<WT, NV, MAXR, NAT>(buf, tabu, n, p.R, u, lane);
             if (j2 >= 0) {
                 ok = true;
                 next = j2;
@@ -1050,7 +1071,7 @@ __device__ __forceinline__ void roulette_steps(const ConstructParams& p, Roulett
 
 // HI: high-occupancy launch (the issue-lean step: in-place scans, predicated
 // sequential group sums)
-template <typename WT, int NV, int MAXR, bool STREAM = false, bool HI = false>
+template <typename WT, int NV, int MAXR, bool STREAM = false, bool HI = false, bool NAT = false>
 __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(ConstructParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
@@ -1063,7 +1084,7 @@ __global__ void __launch_bounds__(32, MAXR == 1 ? 17 : 12) k_construct_roulette(
     for (int kl = blockIdx.x; kl < p.mloc; kl += gridDim.x) {
         RouletteAnt a;
         roulette_begin(p, a, kl, tabu, lane, STREAM);
-        roulette_steps<WT, NV, MAXR, STREAM, HI, HI>(p, a, 1, p.n, smem_raw, phase, fb, fb2);
+        roulette_steps<WT, NV, MAXR, STREAM, HI, HI, NAT>(p, a, 1, p.n, smem_raw, phase, fb, fb2);
         roulette_end(p, a, lane, STREAM);
     }
     if (lane == 0) {

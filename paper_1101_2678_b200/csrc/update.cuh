@@ -491,6 +491,7 @@ struct RowParams {
     unsigned long long* delta_fix; // MODE_DELTA_FIX: n x P64 fixed-point sums
     const long long* stats;        // MODE_DELTA_FIX: stats[7] = the scale exponent s
     int row_begin, row_end;        // k_rows_gather_warp: the rows this launch folds
+    int nat;                       // streamed rows in the natural layout (RowLayout)
 };
 
 // Write one row of the permuted streamed layout (stream_pos) from the natural
@@ -501,13 +502,18 @@ struct RowParams {
 template <int V, typename OT>
 __device__ __forceinline__ void write_stream_row(OT* __restrict__ crow, const double* rowbuf, int n,
                                                  int PW, int C, int LA, int sc, int tid,
-                                                 int nthreads) {
+                                                 int nthreads, bool nat) {
     const int LP = LA + kPad, NVL = C / V, RS = LP * NVL; // vector slots per round
+    nat = nat && (NVL & 1) != 0; // natural layout (RowLayout, odd NV)
     const int nslots = PW / V;
     for (int s = tid; s < nslots; s += nthreads) {
-        const int r = s / RS, rem = s - r * RS;
-        const int t = rem / LP, l = rem - t * LP;
-        const int c0 = r * LA * C + l * C + t * V;
+        int l = 0, c0 = s * V;
+        if (!nat) {
+            const int r = s / RS, rem = s - r * RS;
+            const int t = rem / LP;
+            l = rem - t * LP;
+            c0 = r * LA * C + l * C + t * V;
+        }
         if constexpr (V == 4) {
             float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
             if (l < LA) {
@@ -712,11 +718,11 @@ __global__ void __launch_bounds__(256, MODE == MODE_CHOICE ? 4 : 3) k_rows(RowPa
             const int sc = rmx > 0.0 ? kScaleExp - ilogb(rmx) : 0;
             if (tid == 0) p.scale_exp[i] = sc;
             write_stream_row<4>(p.choice32 + static_cast<size_t>(i) * p.PW, rowbuf, n, p.PW, p.C,
-                                p.LA, sc, tid, blockDim.x); // pads 0
+                                p.LA, sc, tid, blockDim.x, p.nat != 0); // pads 0
         }
         if (p.choice_perm64) {
             write_stream_row<2>(p.choice_perm64 + static_cast<size_t>(i) * p.PW, rowbuf, n, p.PW,
-                                p.C, p.LA, 0, tid, blockDim.x);
+                                p.C, p.LA, 0, tid, blockDim.x, p.nat != 0);
         }
         if (need_sync) __syncthreads();
     }
@@ -846,11 +852,11 @@ __global__ void __launch_bounds__(32) k_rows_gather_warp(RowParams p) {
             const int sc = mx > 0.0 ? kScaleExp - ilogb(mx) : 0;
             if (lane == 0) p.scale_exp[i] = sc;
             write_stream_row<4>(p.choice32 + static_cast<size_t>(i) * p.PW, rowbuf, n, p.PW, p.C,
-                                p.LA, sc, lane, 32);
+                                p.LA, sc, lane, 32, p.nat != 0);
         }
         if (p.choice_perm64) {
             write_stream_row<2>(p.choice_perm64 + static_cast<size_t>(i) * p.PW, rowbuf, n, p.PW,
-                                p.C, p.LA, 0, lane, 32);
+                                p.C, p.LA, 0, lane, 32, p.nat != 0);
         }
         __syncwarp();
     }

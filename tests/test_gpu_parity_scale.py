@@ -110,6 +110,8 @@ def test_late_run_subnormal_regime_tiers_fire_bit_exact(aco, oracle):
             ch = oracle.choice(prob.dist, tau)
             assert np.array_equal(eng.choice(), ch)
             rec = eng.construct()
+            # 384 ants: the plain launch, rows in the natural layout (odd NV)
+            assert ",nat>" in eng.describe()
             tier2 += rec.certified_fp64
             exact += rec.fallbacks
             t_ref, l_ref = par_construct(oracle, prob.dist, ch, 1, it, 0, ants)
