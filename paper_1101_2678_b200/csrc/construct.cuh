@@ -1289,7 +1289,7 @@ __global__ void __launch_bounds__(32) k_construct_roulette_exact(ConstructParams
 // (construction.hpp:108-120), which consumes no draw; it streams the fp64
 // row with 8 independent 16-byte loads per lane in flight.
 #ifndef ACO_NN_MINB
-#define ACO_NN_MINB 28 // resident warps per SM the register budget must allow
+#define ACO_NN_MINB 32 // resident warps per SM the register budget must allow (64 registers, no spills)
 #endif
 // SPEC: the crossing candidate's list is requested before its certification
 // (for latency-bound launches; that variant is held to 64 registers)
