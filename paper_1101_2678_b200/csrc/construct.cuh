@@ -1291,11 +1291,14 @@ __global__ void __launch_bounds__(32) k_construct_roulette_exact(ConstructParams
 #ifndef ACO_NN_MINB
 #define ACO_NN_MINB 32 // resident warps per SM the register budget must allow (64 registers, no spills)
 #endif
+#ifndef ACO_NN_SPEC_MINB
+#define ACO_NN_SPEC_MINB 28 // the same for the latency-bound (SPEC) launches (<= 12 ants per SM)
+#endif
 // SPEC: the crossing candidate's list is requested before its certification
 // (for latency-bound launches; that variant is held to 64 registers)
 // FAST32: nn <= 32 with the row-scaled fp32 list weights (the fast path)
 template <bool SPEC, bool FAST32 = true>
-__global__ void __launch_bounds__(32, SPEC ? 28 : ACO_NN_MINB) k_construct_nn(ConstructParams p) {
+__global__ void __launch_bounds__(32, SPEC ? ACO_NN_SPEC_MINB : ACO_NN_MINB) k_construct_nn(ConstructParams p) {
     extern __shared__ uint32_t smem_tabu[];
     uint32_t* tabu = smem_tabu;
 
