@@ -191,6 +191,7 @@ struct aco_gpu_ctx {
     int32_t* d_succ = nullptr; // [world][n][S]
     int32_t* d_pred = nullptr;
     double* d_delta = nullptr;
+    bool sym = false; // one-GPU accumulate: symmetric upper-triangle delta (k_deposit_sym)
     float* d_delta32 = nullptr; // sharded atomic path over NCCL: the fp32 wire copy of d_delta
     long long* d_stats = nullptr;   // [0..2] stats, [3] best_so_far
     int32_t* d_best = nullptr;      // n+1
@@ -512,11 +513,13 @@ void launch_rows(aco_gpu_ctx* c, int mode) {
         CK(cudaFuncSetAttribute(k_rows<MODE_DELTA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute(k_rows<MODE_DELTA32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute(k_rows<MODE_DELTA_FIX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k_rows<MODE_DELTA_SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
     if (mode == MODE_CHOICE) k_rows<MODE_CHOICE><<<grid, 256, rsmem, c->stream>>>(rp);
     else if (mode == MODE_GATHER) k_rows<MODE_GATHER><<<grid, 256, rsmem, c->stream>>>(rp);
     else if (mode == MODE_DELTA32) k_rows<MODE_DELTA32><<<grid, 256, rsmem, c->stream>>>(rp);
     else if (mode == MODE_DELTA_FIX) k_rows<MODE_DELTA_FIX><<<grid, 256, rsmem, c->stream>>>(rp);
+    else if (mode == MODE_DELTA_SYM) k_rows<MODE_DELTA_SYM><<<grid, 256, rsmem, c->stream>>>(rp);
     else k_rows<MODE_DELTA><<<grid, 256, rsmem, c->stream>>>(rp);
     check_launch(c, "k_rows");
     launch_topk(c);
@@ -1229,6 +1232,17 @@ void do_update(aco_gpu_ctx* c) {
         CK(cudaEventRecord(c->ev[4], c->stream));
     } else {
         const size_t count2 = static_cast<size_t>(c->n) * c->P64 / 2;
+        if (c->sym) {
+            // evaporation fused into k_rows<MODE_DELTA_SYM>; one red per edge
+            CK(cudaMemsetAsync(c->d_delta, 0, static_cast<size_t>(c->n) * c->P64 * sizeof(double), c->stream));
+            k_deposit_sym<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_tours, c->d_inv, c->n, c->P64,
+                                                                 c->mloc, c->d_delta);
+            check_launch(c, "k_deposit_sym");
+            CK(cudaEventRecord(c->ev[4], c->stream));
+            launch_rows(c, MODE_DELTA_SYM);
+            CK(cudaEventRecord(c->ev[5], c->stream));
+            return;
+        }
         k_evaporate<<<c->num_sms * 8, 256, 0, c->stream>>>(c->d_tau, count2, keep);
         check_launch(c, "k_evaporate");
         if (c->d_dnn) { // nn selection: list edges through the compact slots
@@ -1605,7 +1619,9 @@ aco_status aco_gpu_create(const aco_gpu_params* prm, const int32_t* dist, aco_gp
         c->row_shard = c->sharded && c->world > 1 && warp_gather && !(gsplit && gsplit[0] == '0') &&
                        !(rsh && rsh[0] == '0');
         c->row_blk = c->row_shard ? (n + c->world - 1) / c->world : n;
-        if ((c->sharded && c->cfg.deposit == ACO_DEP_ACCUMULATE && !c->fixed) ||
+        c->sym = ACO_SYM_DEPOSIT && !c->sharded && !c->fixed && c->cfg.deposit == ACO_DEP_ACCUMULATE &&
+                 c->cfg.selection != ACO_SEL_NN;
+        if ((c->sharded && c->cfg.deposit == ACO_DEP_ACCUMULATE && !c->fixed) || c->sym ||
             (warp_gather && !(gsplit && gsplit[0] == '0'))) {
             // row-sharded: world row blocks of row_blk rows (the last one padded)
             const size_t dcells = std::max(cells, static_cast<size_t>(c->world) * c->row_blk * c->P64);

@@ -279,6 +279,24 @@ __global__ void k_deposit_atomic(const int32_t* __restrict__ tours, const double
     }
 }
 
+// Symmetric accumulate deposit (one-GPU roulette / data-parallel): the
+// reference adds w_k to tau[a][b] AND tau[b][a] (pheromone.hpp:198-205), two
+// equal sums, so one red per edge into the upper-triangle cell of a cleared
+// delta carries both; k_rows<MODE_DELTA_SYM> applies it to both cells after
+// the evaporation (the atomic path's 1e-5 relative contract: the same sums,
+// associated differently).
+__global__ void k_deposit_sym(const int32_t* __restrict__ tours, const double* __restrict__ inv,
+                              int n, int P64, int mloc, double* __restrict__ delta) {
+    const size_t total = static_cast<size_t>(mloc) * n;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int kl = static_cast<int>(i / n), s = static_cast<int>(i - static_cast<size_t>(kl) * n);
+        const int32_t* t = tours + static_cast<size_t>(kl) * (n + 1);
+        const int a = t[s], b = t[s + 1];
+        atomicAdd(delta + static_cast<size_t>(min(a, b)) * P64 + max(a, b), inv[kl]);
+    }
+}
+
 // Accumulate deposit for the nn selection (config 5).  An edge a -> b whose
 // head is member q of a's nn list (the construction recorded q) adds w_k to
 // the compact slot dnn[a][q] — n x nn doubles, 2.4 MB at 10k, L2-resident —
@@ -463,7 +481,15 @@ __global__ void k_mc_barrier(unsigned long long* mc_flag, const unsigned long lo
 // wire; k_delta_pack already zeroed the fp64 delta)
 // MODE_DELTA_FIX: tau = fl(fl(tau*keep) + delta_i64 * 2^-s) from the exact
 // fixed-point sums (k_deposit_fixed), then clears the delta.
-enum { MODE_CHOICE = 0, MODE_GATHER = 1, MODE_DELTA = 2, MODE_DELTA32 = 3, MODE_DELTA_FIX = 4 };
+#ifndef ACO_SYM_DEPOSIT
+#define ACO_SYM_DEPOSIT 1 // one-GPU accumulate through the symmetric upper-triangle delta
+#endif
+// MODE_DELTA_SYM: MODE_DELTA over a symmetric delta kept in the upper
+// triangle only (k_deposit_sym: one red per edge instead of two): row i reads
+// delta[i][j] for j > i and the column delta[j][i] for j < i; the buffer is
+// cleared before the deposit (a cell is read by two rows, so no row can clear it)
+enum { MODE_CHOICE = 0, MODE_GATHER = 1, MODE_DELTA = 2, MODE_DELTA32 = 3, MODE_DELTA_FIX = 4,
+       MODE_DELTA_SYM = 5 };
 
 struct RowParams {
     double* tau;             // n x P64
@@ -637,7 +663,7 @@ __global__ void __launch_bounds__(256, MODE == MODE_CHOICE ? 4 : 3) k_rows(RowPa
             p.etab ? reinterpret_cast<const double2*>(p.etab + static_cast<size_t>(i) * p.P64) : nullptr;
         double2* trow2 = reinterpret_cast<double2*>(trow);
         double2* crow2 = reinterpret_cast<double2*>(p.choice64 + static_cast<size_t>(i) * p.P64);
-        double2* drw2 = MODE == MODE_DELTA
+        double2* drw2 = (MODE == MODE_DELTA || MODE == MODE_DELTA_SYM)
                             ? reinterpret_cast<double2*>(p.delta + static_cast<size_t>(i) * p.P64)
                             : nullptr;
         ulonglong2* dfx2 = MODE == MODE_DELTA_FIX
@@ -654,6 +680,14 @@ __global__ void __launch_bounds__(256, MODE == MODE_CHOICE ? 4 : 3) k_rows(RowPa
                 tv[u] = in ? trow2[j2] : make_double2(0.0, 0.0);
                 dv[u] = (in && !erow2) ? __ldg(drow2 + j2) : make_int2(0, 0);
                 if constexpr (MODE == MODE_DELTA) dl[u] = in ? drw2[j2] : make_double2(0.0, 0.0);
+                if constexpr (MODE == MODE_DELTA_SYM) {
+                    const int j = 2 * j2;
+                    const double2 up = (in && j + 1 > i) ? drw2[j2] : make_double2(0.0, 0.0);
+                    const double lx = (in && j < i) ? p.delta[static_cast<size_t>(j) * p.P64 + i] : 0.0;
+                    const double ly = (in && j + 1 < i) ? p.delta[static_cast<size_t>(j + 1) * p.P64 + i] : 0.0;
+                    dl[u] = make_double2(j < i ? lx : (j > i ? up.x : 0.0),
+                                         j + 1 < i ? ly : (j + 1 > i ? up.y : 0.0));
+                }
                 if constexpr (MODE == MODE_DELTA_FIX) {
                     const ulonglong2 f = in ? dfx2[j2] : make_ulonglong2(0ull, 0ull);
                     // exact integer sum -> double (one rounding) -> exact 2^-s scaling
@@ -684,7 +718,7 @@ __global__ void __launch_bounds__(256, MODE == MODE_CHOICE ? 4 : 3) k_rows(RowPa
                     const int j = 2 * j2;
                     double2 t = tv[u];
                     if constexpr (MODE == MODE_GATHER || MODE == MODE_DELTA || MODE == MODE_DELTA32 ||
-                                  MODE == MODE_DELTA_FIX) {
+                                  MODE == MODE_DELTA_FIX || MODE == MODE_DELTA_SYM) {
                         // pheromone.hpp:183 (evaporate) then :220 / the summed delta
                         t.x = __dadd_rn(__dmul_rn(t.x, p.keep), dl[u].x);
                         t.y = __dadd_rn(__dmul_rn(t.y, p.keep), dl[u].y);
