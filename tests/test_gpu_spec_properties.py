@@ -92,6 +92,25 @@ def test_tau_symmetry_and_deposit_conservation(aco):
             assert abs(mass - expect) <= 1e-9 * expect
 
 
+@pytest.mark.parametrize("selection", [0, 2])
+def test_accumulate_one_gpu_symmetric_and_conserving(aco, selection):
+    """One-GPU accumulate (k_deposit_sym + k_rows<DELTA_SYM>): both cells of an
+    edge receive the same fl(fl(tau*keep) + delta), so tau stays EXACTLY
+    symmetric; the deposited mass matches sum_k 2n/C_k to rounding."""
+    n = 300
+    prob, eng = _engine(aco, aco.synthetic_instance(n), deposit=0, selection=selection)
+    with eng:
+        for it in range(4):
+            before = eng.pheromone()
+            eng.run_iteration()
+            after = eng.pheromone()
+            assert np.array_equal(after, after.T), f"asymmetric at iteration {it}"
+            _, lens = eng.ants()
+            mass = (after - before * 0.5).sum()
+            expect = (2.0 * n / lens.astype(np.float64)).sum()
+            assert abs(mass - expect) <= 1e-9 * expect
+
+
 @pytest.mark.parametrize("deposit", [1, 0])
 def test_determinism(aco, deposit):
     """Same configuration and seed, two engines: identical tours, lengths and
