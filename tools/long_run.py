@@ -8,4 +8,4 @@ eng = aco.Engine(prob, aco.RunConfig(params=aco.Parameters(m=0, seed=1), selecti
 for it in range(300):
     r = eng.run_iteration()
     if it % 25 == 0 or it == 299:
-        print(json.dumps({"it": it, "kernel_ms": round(r.construct_kernel_ms, 3), "update_ms": round(r.update_ms, 3), "fallbacks": r.fallbacks, "best": r.best_length}), flush=True)
+        print(json.dumps({"it": it, "kernel_ms": round(r.construct_kernel_ms, 3), "update_ms": round(r.update_ms, 3), "fallbacks": r.fallbacks, "tier2": r.certified_fp64, "best": r.best_length}), flush=True)
